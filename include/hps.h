@@ -109,7 +109,7 @@ typedef struct HpsArgmin {
   uint64_t evaluated;   /* plans scored */
   uint64_t feasible;    /* plans with status OK */
   uint32_t status;      /* status of the winner */
-  uint32_t pad;
+  uint32_t flags;       /* bit0: some plan hit HPS_ST_NO_CPU_TYPE, bit1: HPS_ST_INVALID */
 } HpsArgmin;
 
 /* numpy PCG64 bit-generator state (np.random.PCG64().state) as four 64-bit words */
@@ -139,6 +139,13 @@ int hps_score_plans(HpsInstance* inst, const uint8_t* d_plans, int64_t n,
 int hps_enum_argmin(HpsInstance* inst, uint64_t begin, uint64_t end, int32_t feasible_only,
                     HpsArgmin* d_best, void* stream);
 
+/* Argmin over an explicit plan batch (u8 [n][L] device memory), same key and tie rules as
+ * hps_enum_argmin; the rank packs ceil(log2 T) bits per layer (needs bits*L <= 128).
+ * Replaces the scoring loop + _better of random_search's dedup path and of any caller that
+ * already holds its plans (ls/baselines.py:252-282). */
+int hps_plans_argmin(HpsInstance* inst, const uint8_t* d_plans, int64_t n, int32_t feasible_only,
+                     HpsArgmin* d_best, void* stream);
+
 /* Random sweep: plan p (p in [first, first+n)) is the p-th call of
  * default_rng(seed).integers(0, T, L) (ls/baselines.py:270-271) from `gen`'s initial state.
  * Penalised plans are included (ls/baselines.py:275-278). Requires a power-of-two T
@@ -157,6 +164,10 @@ int hps_report(HpsInstance* inst, const uint8_t* d_plans, const int32_t* d_k,
                const int32_t* d_ps, int64_t n, double* d_ct, double* d_dt, double* d_et,
                double* d_tp, double* d_pipeline_tp, double* d_exec_time, double* d_cost,
                uint8_t* d_feasible, void* stream);
+
+/* FP64 pipe microbenchmark (kind 0: dependent-chain DFMA x8 per thread, 16 flops per loop
+ * step per chain pair; kind 1: IEEE division). Used for the roofline denominator. */
+int hps_probe_fp64(int kind, double* d_out, int blocks, int threads, int iters, void* stream);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,8 @@ typedef struct {
   int tot_type[MAXT + 1];
   int64_t tot_count[MAXT + 1];
   double pipeline_tp, exec_time;
+  int nraw;   /* breakpoints before dedup (diagnostic) */
+  int nspan;  /* sum over stages of (span+1) for spans <= 4096, plus 2 */
 } HpsoResult;
 
 /* ---- Python builtin sum() over floats with int start 0 (CPython 3.12 Neumaier) ---- */
@@ -568,6 +570,8 @@ static void score_plan(const HpsInstanceDesc* d, const uint8_t* plan, Scratch* w
         if (e >= tau_lo && e <= tau_hi) cand[nc++] = e;
       }
     }
+    r->nraw = (int)nc;
+    r->nspan = (int)nb;
     qsort(cand, nc, sizeof(double), cmp_double);
     size_t u = 0;
     for (size_t i = 0; i < nc; i++)

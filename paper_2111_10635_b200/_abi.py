@@ -54,7 +54,7 @@ class HpsPlanResults(C.Structure):
 class HpsArgmin(C.Structure):
     _fields_ = [("cost", C.c_double), ("rank_hi", C.c_uint64), ("rank_lo", C.c_uint64),
                 ("evaluated", C.c_uint64), ("feasible", C.c_uint64),
-                ("status", C.c_uint32), ("pad", C.c_uint32)]
+                ("status", C.c_uint32), ("flags", C.c_uint32)]
 
 
 class HpsPcg64(C.Structure):
@@ -131,10 +131,13 @@ _SIGNATURES = {
                                   C.POINTER(HpsPlanResults), C.c_void_p]),
     "hps_enum_argmin": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int32, C.c_void_p,
                                   C.c_void_p]),
+    "hps_plans_argmin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                   C.c_void_p]),
     "hps_random_argmin": (C.c_int, [C.c_void_p, C.POINTER(HpsPcg64), C.c_uint64, C.c_uint64,
                                     C.c_void_p, C.c_void_p]),
     "hps_random_plans": (C.c_int, [C.c_void_p, C.POINTER(HpsPcg64), C.c_uint64, C.c_uint64,
                                    C.c_void_p, C.c_void_p]),
+    "hps_probe_fp64": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),
 }
 

@@ -1,0 +1,216 @@
+// hps_device.cuh — device-side data layout and exact arithmetic primitives of the plan
+// evaluator. Compiled with --fmad=false and IEEE division/sqrt so every operation below
+// rounds exactly like CPython/numpy binary64 (the bit-exact contract of SURVEY.md §7).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hps.h"
+
+namespace hps {
+
+typedef unsigned __int128 u128;
+
+constexpr int kMaxL = HPS_MAX_LAYERS;
+constexpr int kMaxT = HPS_MAX_TYPES;
+constexpr int kBpLimit = HPS_BREAKPOINT_LIMIT;
+constexpr int kWarp = 32;
+
+// Aggregates of one stage = maximal run (type t, layers first..last), as build_stages makes
+// them (ls/domain.py:275-328), plus the constants every formula of ls/provisioner.py needs.
+struct __align__(16) StageEntry {
+  double c_oct;   // oct / B_o
+  double c_odt;   // odt / B_o
+  double alpha;
+  double beta;
+  double oma;     // 1.0 - alpha
+  double omb;     // 1.0 - beta
+  double oct;     // Neumaier sum of member oct (ls/domain.py:306)
+  double odt;     // last member's odt (ls/domain.py:324)
+  double serial;  // max((oct/B_o)(1-alpha), (odt/B_o)(1-beta))  (ls/provisioner.py:184-193)
+  int32_t valid;  // 0 when a member lacks a profile for the type (PlanValidationError)
+  int32_t type;
+};
+
+// Stage-0 exits of optimize_k1 for an entry starting at layer 0 (ls/provisioner.py:394-397)
+struct Stage0Info {
+  double tau_hi;  // min(B/limit, et(stage0, k1_floor)) if k1_floor > 1
+  double gap;     // InfeasibleError gap when status == HPS_ST_MIN_K1
+  int32_t status; // HPS_ST_OK or HPS_ST_MIN_K1
+  int32_t pad;
+};
+
+// Immutable per-instance constants, in __constant__-friendly form (passed by value).
+struct InstanceConsts {
+  int32_t L, T, P;        // P = L(L+1)/2 stage ranges per type
+  int32_t with_ps;
+  int32_t ps_type;        // cheapest CPU type (ls/domain.py:163-167), -1 if none
+  int32_t newton_max_iters;
+  double bo, batch, work, limit;
+  double penalty_scale;   // 1e6 * max price (ls/scoring.py:47-50)
+  double ps_cores_per_gpu, newton_tol, fd_step;
+  double tau_limit;       // B / limit (ls/provisioner.py:395)
+  double price_s[kMaxT];  // price_per_hour / 3600.0 (ls/provisioner.py:209)
+  double price_h[kMaxT];  // price_per_hour
+  int64_t quota[kMaxT];
+  uint8_t is_cpu[kMaxT];
+  int32_t et_cap[kMaxT];  // ET table holds m in [1, et_cap[t]] for stages of type t
+  int64_t et_off[kMaxT];  // ET table offset of type t's block (rows of et_cap[t])
+};
+
+struct DeviceTables {
+  const StageEntry* stages;   // [T * P]
+  const Stage0Info* stage0;   // [T * L] indexed by (t, last)
+  const double* et;           // ET[e][m-1] = max(ct, dt) at integer count m
+  const int32_t* cls;         // [T * P] ET-equivalence class: entries with bitwise-equal
+                              // (oct, odt, alpha, beta) share counts and breakpoints
+};
+
+__device__ __forceinline__ int tb_class(const DeviceTables& tb, int e) { return __ldg(tb.cls + e); }
+
+__host__ __device__ __forceinline__ int pair_index(int first, int last) {
+  return last * (last + 1) / 2 + first;
+}
+__host__ __device__ __forceinline__ int entry_index(int P, int t, int first, int last) {
+  return t * P + pair_index(first, last);
+}
+
+// Python max(a, b) / min(a, b): the first argument unless the second is strictly better.
+__device__ __forceinline__ double pmax(double a, double b) { return (b > a) ? b : a; }
+__device__ __forceinline__ double pmin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double clamp_gap(double g) { return (g > 0.0) ? g : 0.0; }
+
+// _stage_et (ls/provisioner.py:144-147) == compute_ct/compute_dt + max (ls/costmodel.py:50-66)
+__device__ __forceinline__ double stage_et(const StageEntry& s, double k) {
+  double ct = s.c_oct * (s.oma + s.alpha / k);
+  double dt = s.c_odt * (s.omb + s.beta / k);
+  return pmax(ct, dt);
+}
+
+// _floor_count (ls/provisioner.py:150-176): false on InfeasibleError (gap = -headroom).
+__device__ __forceinline__ bool floor_count(const StageEntry& s, double tau, double bo,
+                                            double& req, double& gap) {
+  double required = 1.0;
+  if (s.oct != 0) {
+    double h = tau * bo / s.oct - s.oma;
+    if (s.alpha == 0.0) {
+      if (!(h >= 0)) { gap = clamp_gap(-h); return false; }
+    } else {
+      if (h <= 0) { gap = clamp_gap(-h); return false; }
+      required = pmax(required, s.alpha / h);
+    }
+  }
+  if (s.odt != 0) {
+    double h = tau * bo / s.odt - s.omb;
+    if (s.beta == 0.0) {
+      if (!(h >= 0)) { gap = clamp_gap(-h); return false; }
+    } else {
+      if (h <= 0) { gap = clamp_gap(-h); return false; }
+      required = pmax(required, s.beta / h);
+    }
+  }
+  req = required;
+  return true;
+}
+
+// _iceil (ls/provisioner.py:75-77) as an integer-valued double (Python int semantics)
+__device__ __forceinline__ double iceil(double x) {
+  double c = ceil(x - 1e-9);
+  return c < 1.0 ? 1.0 : c;
+}
+
+// integer count at tau, +inf when _floor_count raises
+__device__ __forceinline__ double count_at(const StageEntry& s, double tau, double bo) {
+  double r, g;
+  return floor_count(s, tau, bo, r, g) ? iceil(r) : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+__device__ __forceinline__ double et_lookup(const InstanceConsts& c, const DeviceTables& tb,
+                                            const StageEntry& s, int e, double k) {
+  const int t = s.type;
+  if (k <= (double)c.et_cap[t]) {
+    const int64_t pe = e - t * c.P;  // entry within type block
+    return __ldg(tb.et + c.et_off[t] + pe * (int64_t)c.et_cap[t] + ((int64_t)k - 1));
+  }
+  return stage_et(s, k);
+}
+
+__device__ __forceinline__ uint64_t sat_count(double k) {  // saturating u64 of a count
+  return (k < 1.125899906842624e15) ? (uint64_t)k : (uint64_t)1125899906842624ULL;  // 2^50
+}
+
+// Exact u128 of an integer-valued double in [1, 2^127) (Python int(count)).
+__device__ __forceinline__ u128 dbl_to_u128(double x) {
+  if (!(x < 1.7014118346046923e38)) return ~(u128)0 >> 1;
+  int e;
+  double m = frexp(x, &e);
+  uint64_t mi = (uint64_t)ldexp(m, 53);
+  return (e >= 53) ? ((u128)mi << (e - 53)) : ((u128)mi >> (53 - e));
+}
+
+// Python int/int true division (correctly rounded), 0 <= n < 2^127, d > 0.
+__device__ inline double int_true_div(u128 n, int64_t d) {
+  if (n < ((u128)1 << 53)) return (double)(uint64_t)n / (double)d;
+  u128 q = n / (u128)d, r = n % (u128)d;
+  int e = 0;
+  u128 mant = q;
+  while ((mant >> 54) == 0) {
+    r <<= 1;
+    mant = (mant << 1) | (r >= (u128)d ? 1u : 0u);
+    if (r >= (u128)d) r -= (u128)d;
+    e--;
+  }
+  bool sticky = (r != 0);
+  int nb = 0;
+  for (u128 t = mant; t; t >>= 1) nb++;
+  int drop = nb - 53;
+  u128 low = mant & ((((u128)1) << drop) - 1);
+  u128 half = ((u128)1) << (drop - 1);
+  mant >>= drop;
+  e += drop;
+  if (low > half || (low == half && (sticky || (mant & 1)))) mant += 1;
+  return ldexp((double)(uint64_t)mant, e);
+}
+
+// CPython 3.12 builtin sum() over floats with int start (Neumaier), sequential.
+struct PySum {
+  double f = 0.0, c = 0.0;
+  bool started = false;
+  __device__ __forceinline__ void add(double x) {
+    if (!started) { f = 0.0 + x; started = true; return; }
+    double t = f + x;
+    if (fabs(f) >= fabs(x)) c += (f - t) + x; else c += (x - t) + f;
+    f = t;
+  }
+  __device__ __forceinline__ double result() const {
+    if (!started) return 0.0;
+    return (c != 0.0 && isfinite(c)) ? f + c : f;
+  }
+};
+
+// ---- numpy PCG64 (XSL-RR 128/64) ----
+__host__ __device__ __forceinline__ u128 pcg_mult() {
+  return (((u128)0x2360ED051FC65DA4ULL) << 64) | 0x4385DF649FCCF645ULL;
+}
+__device__ __forceinline__ uint64_t pcg_output(u128 s) {
+  uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+  uint64_t x = hi ^ lo;
+  unsigned rot = (unsigned)(hi >> 58);
+  return (x >> rot) | (x << ((64 - rot) & 63));
+}
+// state after `delta` steps (LCG jump-ahead by squaring)
+__host__ __device__ inline u128 pcg_advance(u128 state, u128 inc, u128 delta) {
+  u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+}  // namespace hps

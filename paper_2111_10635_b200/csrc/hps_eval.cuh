@@ -1,0 +1,437 @@
+// hps_eval.cuh — warp-per-plan evaluation of one scheduling plan (the body of
+// PlanScorer.__call__, ls/scoring.py:79-101), shared by the scoring, enumeration and
+// random-sweep kernels.
+//
+// Work split inside a warp (32 lanes, one plan):
+//   * stage construction: lane s owns stage s (and s+32): runs from a ballot over layer
+//     boundaries, aggregates from the instance stage table (exact Neumaier sums done once);
+//   * optimize_k1 exits + 60-step quota bisection (ls/provisioner.py:394-437): lanes evaluate
+//     their stages' counts in parallel; a stage whose count is pinned by monotonicity
+//     (count(b) == count(a)) is not re-evaluated;
+//   * _best_candidate (ls/provisioner.py:262-314): the breakpoint candidates are spread over
+//     lanes; each lane keeps a Pareto buffer of near-minimal (cost, tau) pairs and the warp
+//     merges them. Candidates are never sorted: the reference's choice (minimum cost, then the
+//     lexicographically smallest count vector among costs <= best + 1e-15) is a function of
+//     the candidate SET, and counts are non-increasing in tau, so "lexicographically smallest"
+//     == "largest tau among the ties".
+//   * quota feasibility of candidates needs no work: every candidate lies in [tau_lo, tau_hi]
+//     where counts are <= count(tau_lo), which passed quota_ok.
+#pragma once
+#include "hps_device.cuh"
+
+namespace hps {
+
+constexpr int kTieBuf = 4;
+constexpr uint8_t kStPending = 0xFE;  // internal: needs the block-per-plan slow path
+
+template <int MAXS>
+struct WarpSmem {
+  StageEntry st[MAXS];
+  double kmin[MAXS];   // count at tau_hi  (m_min, ls/provisioner.py:444)
+  double kmax[MAXS];   // count at tau_lo  (m_max, ls/provisioner.py:445)
+  double kres[MAXS];   // final counts
+  int32_t ent[MAXS];   // stage-table entry
+  int32_t cls[MAXS];   // ET-equivalence class of the entry
+  int32_t pre[MAXS + 1];  // exclusive prefix of candidate counts over class leaders
+  unsigned long long tsum[kMaxT];
+};
+
+struct PlanOut {
+  double cost, gap;
+  int status;  // HPS_ST_* | overflow flag, or kStPending
+  int S;
+  int ps;
+};
+
+struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min + 1e-15
+  double c[kTieBuf], t[kTieBuf];
+  int n;
+  bool overflow;
+  double mn;
+  __device__ __forceinline__ void init() { n = 0; overflow = false; mn = __longlong_as_double(0x7ff0000000000000LL); }
+  __device__ __forceinline__ void insert(double cost, double tau) {
+    if (!(cost <= mn + 1e-15) && n > 0) return;  // cannot be within 1e-15 of the minimum
+    if (cost < mn) {
+      mn = cost;
+      const double lim = mn + 1e-15;
+      int m = 0;
+      for (int i = 0; i < n; i++)
+        if (c[i] <= lim) { c[m] = c[i]; t[m] = t[i]; m++; }
+      n = m;
+    }
+    // dominated by an existing entry (cheaper-or-equal and later-or-equal)?
+    for (int i = 0; i < n; i++)
+      if (c[i] <= cost && t[i] >= tau) return;
+    int m = 0;
+    for (int i = 0; i < n; i++)
+      if (!(cost <= c[i] && tau >= t[i])) { c[m] = c[i]; t[m] = t[i]; m++; }
+    n = m;
+    if (n == kTieBuf) { overflow = true; return; }
+    c[n] = cost; t[n] = tau; n++;
+  }
+  // largest tau whose cost is <= lim (the lexicographically smallest vector among ties)
+  __device__ __forceinline__ double best_tau(double lim) const {
+    double bt = -__longlong_as_double(0x7ff0000000000000LL);
+    for (int i = 0; i < n; i++)
+      if (c[i] <= lim && t[i] > bt) bt = t[i];
+    return bt;
+  }
+};
+
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Evaluate one candidate tau: numpy _best_candidate column (ls/provisioner.py:286-308).
+// Returns +inf when the column is not ok (throughput <= limit).
+template <int MAXS>
+__device__ __forceinline__ double candidate_cost(const InstanceConsts& c, const DeviceTables& tb,
+                                                 const WarpSmem<MAXS>& w, int S, double tau) {
+  double E = 0.0, P = 0.0;
+  for (int r = 0; r < S; r++) {
+    const StageEntry& s = w.st[r];
+    double k = w.kmin[r];
+    if (w.kmax[r] != k) k = count_at(s, tau, c.bo);
+    double et = et_lookup(c, tb, s, w.ent[r], k);
+    double term = c.price_s[s.type] * k;
+    if (r == 0) { E = et; P = term; } else { E = fmax(E, et); P = P + term; }
+  }
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double thr = (E > 0) ? c.batch / E : inf;
+  if (!(thr > c.limit)) return inf;
+  return c.work / thr * P;
+}
+
+// Phase A: stages, optimize_k1 exits and the bisection. Returns false when the plan is
+// finished (infeasible / invalid); otherwise fills w.kmin/kmax and tau_lo/tau_hi.
+// Lane l holds digits d0 (layer l) and d1 (layer l+32).
+template <int MAXS>
+__device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables& tb,
+                                    WarpSmem<MAXS>& w, int d0, int d1, PlanOut& out,
+                                    double& tau_lo_out, double& tau_hi_out, int& n_cand) {
+  const int lane = threadIdx.x & 31;
+  const int L = c.L;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  // --- runs (ls/domain.py:293-296): stage starts where the type changes ---
+  int prev0 = __shfl_up_sync(0xffffffffu, d0, 1);
+  int last_lo = __shfl_sync(0xffffffffu, d0, 31);
+  int prev1 = __shfl_up_sync(0xffffffffu, d1, 1);
+  if (lane == 0) prev1 = last_lo;
+  bool start0 = (lane < L) && (lane == 0 || d0 != prev0);
+  bool start1 = (lane + 32 < L) && (d1 != prev1);
+  unsigned m0 = __ballot_sync(0xffffffffu, start0), m1 = __ballot_sync(0xffffffffu, start1);
+  bool bad_digit = (lane < L && (d0 < 0 || d0 >= c.T)) || (lane + 32 < L && (d1 < 0 || d1 >= c.T));
+  if (__any_sync(0xffffffffu, bad_digit)) {
+    out.status = HPS_ST_INVALID; out.cost = __longlong_as_double(0x7ff8000000000000LL); out.gap = 0; out.S = 0;
+    return false;
+  }
+  const int c0 = __popc(m0);
+  const int S = c0 + __popc(m1);
+  out.S = S;
+  // lane s builds stage s and s+32
+  bool invalid = false;
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    int first = -1, last = -1;
+    if (s < S) {
+      first = (s < c0) ? (int)__fns(m0, 0, s + 1) : 32 + (int)__fns(m1, 0, s - c0 + 1);
+      int nx = s + 1;
+      if (nx < S) last = ((nx < c0) ? (int)__fns(m0, 0, nx + 1) : 32 + (int)__fns(m1, 0, nx - c0 + 1)) - 1;
+      else last = L - 1;
+    }
+    int src = first & 31;
+    int t0 = __shfl_sync(0xffffffffu, d0, src), t1 = __shfl_sync(0xffffffffu, d1, src);
+    if (s < S) {
+      const int type = (first < 32) ? t0 : t1;
+      const int e = entry_index(c.P, type, first, last);
+      w.st[s] = tb.stages[e];
+      w.ent[s] = e;
+      invalid |= (w.st[s].valid == 0);
+    }
+  }
+  __syncwarp();
+  if (__any_sync(0xffffffffu, invalid)) {
+    out.status = HPS_ST_INVALID; out.cost = __longlong_as_double(0x7ff8000000000000LL); out.gap = 0;
+    return false;
+  }
+  // --- stage-0 bound and tau_hi (ls/provisioner.py:394-397) ---
+  const int type0 = w.st[0].type;
+  const int last0 = (S > 1) ? ((1 < c0) ? (int)__fns(m0, 0, 2) : 32 + (int)__fns(m1, 0, 1)) - 1 : L - 1;
+  const Stage0Info s0 = tb.stage0[type0 * L + last0];
+  if (s0.status != HPS_ST_OK) {
+    out.status = s0.status; out.gap = s0.gap; out.cost = c.penalty_scale * (1.0 + pmax(0.0, s0.gap));
+    return false;
+  }
+  const double tau_hi = s0.tau_hi;
+  // --- serial floor (ls/provisioner.py:399-412) ---
+  double ser = 0.0;
+  for (int s = lane; s < S; s += 32) ser = fmax(ser, w.st[s].serial);
+  ser = warp_max(ser);
+  if (ser >= tau_hi) {
+    out.status = HPS_ST_SERIAL; out.gap = clamp_gap((ser - tau_hi) / tau_hi);
+    out.cost = c.penalty_scale * (1.0 + pmax(0.0, out.gap));
+    return false;
+  }
+  // --- counts at tau_hi + quota (ls/provisioner.py:413-427) ---
+  if (lane < kMaxT) w.tsum[lane] = 0ull;
+  __syncwarp();
+  double kb[2] = {inf, inf}, ka[2] = {inf, inf}, gapv[2] = {0.0, 0.0};
+  bool raised[2] = {false, false};
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s < S) {
+      double r;
+      if (floor_count(w.st[s], tau_hi, c.bo, r, gapv[slot])) {
+        kb[slot] = iceil(r);
+        atomicAdd(&w.tsum[w.st[s].type], sat_count(kb[slot]));
+      } else {
+        raised[slot] = true;
+      }
+    }
+  }
+  __syncwarp();
+  bool over = (lane < c.T) && (w.tsum[lane] > (unsigned long long)c.quota[lane]);
+  unsigned over_mask = __ballot_sync(0xffffffffu, over);
+  unsigned r0 = __ballot_sync(0xffffffffu, raised[0]), r1 = __ballot_sync(0xffffffffu, raised[1]);
+  if (r0 | r1 | over_mask) {
+    if (r0 | r1) {  // _counts_at(tau_hi) raises from the first raising stage (:414)
+      int src = r0 ? (__ffs(r0) - 1) : (__ffs(r1) - 1);
+      double g = __shfl_sync(0xffffffffu, r0 ? gapv[0] : gapv[1], src);
+      out.status = HPS_ST_FLOOR_TAU_HI; out.gap = g;
+    } else {  // first offending type in ascending id (:418-420), exact Python-int totals
+      for (int slot = 0; slot < 2; slot++) {
+        const int s = lane + 32 * slot;
+        if (s < S) w.kres[s] = kb[slot];
+      }
+      __syncwarp();
+      const int off = __ffs(over_mask) - 1;
+      double g = 0.0;
+      if (lane == 0) {
+        u128 tot = 0;
+        for (int s = 0; s < S; s++)
+          if (w.st[s].type == off) tot += dbl_to_u128(w.kres[s]);
+        g = clamp_gap(int_true_div(tot - (u128)c.quota[off], c.quota[off]));
+      }
+      out.status = HPS_ST_QUOTA_TAU_HI; out.gap = __shfl_sync(0xffffffffu, g, 0);
+    }
+    out.cost = c.penalty_scale * (1.0 + pmax(0.0, out.gap));
+    return false;
+  }
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s < S) w.kmin[s] = kb[slot];
+  }
+  // --- bisection (ls/provisioner.py:430-437); counts monotone in tau => pinning ---
+  double a = ser, b = tau_hi;
+  for (int it = 0; it < 60; it++) {
+    const double mid = (a + b) / 2.0;
+    double km[2] = {inf, inf};
+    bool rz = false;
+    if (lane < kMaxT) w.tsum[lane] = 0ull;
+    __syncwarp();
+    for (int slot = 0; slot < 2; slot++) {
+      const int s = lane + 32 * slot;
+      if (s < S) {
+        km[slot] = (ka[slot] == kb[slot]) ? kb[slot] : count_at(w.st[s], mid, c.bo);
+        if (km[slot] == inf) rz = true; else atomicAdd(&w.tsum[w.st[s].type], sat_count(km[slot]));
+      }
+    }
+    __syncwarp();
+    bool bad = rz || ((lane < c.T) && (w.tsum[lane] > (unsigned long long)c.quota[lane]));
+    const bool ok = !__any_sync(0xffffffffu, bad);
+    if (ok) { b = mid; kb[0] = km[0]; kb[1] = km[1]; }
+    else { a = mid; ka[0] = km[0]; ka[1] = km[1]; }
+  }
+  const double tau_lo = b;
+  // --- m_min / m_max and class leaders (ls/provisioner.py:442-455) ---
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s < S) {
+      w.kmax[s] = kb[slot];
+      w.cls[s] = tb_class(tb, w.ent[s]);
+    }
+  }
+  __syncwarp();
+  // candidate count over class leaders (identical (oct,odt,alpha,beta) => identical counts
+  // and breakpoints, so only the first stage of a class contributes distinct values)
+  int cnt[2] = {0, 0};
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s < S) {
+      bool leader = true;
+      for (int q = 0; q < s; q++)
+        if (w.cls[q] == w.cls[s]) { leader = false; break; }
+      double span = w.kmax[s] - w.kmin[s];
+      if (leader && span <= (double)kBpLimit) cnt[slot] = (int)span + 1;
+    }
+  }
+  // exclusive prefix over s = 0..S-1 (slot 0 then slot 1)
+  int inc0 = cnt[0];
+  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, inc0, o); if (lane >= o) inc0 += v; }
+  int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+  int inc1 = cnt[1];
+  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, inc1, o); if (lane >= o) inc1 += v; }
+  int tot1 = __shfl_sync(0xffffffffu, inc1, 31);
+  if (lane < S) w.pre[lane] = inc0 - cnt[0];
+  if (lane + 32 < S) w.pre[lane + 32] = tot0 + inc1 - cnt[1];
+  if (lane == 0) w.pre[S] = tot0 + tot1;
+  __syncwarp();
+  n_cand = tot0 + tot1 + 2;
+  tau_lo_out = tau_lo;
+  tau_hi_out = tau_hi;
+  return true;
+}
+
+}  // namespace hps
+
+namespace hps {
+
+// Phase B: _best_candidate over the implicit candidate set {tau_lo, tau_hi} U breakpoints of
+// class leaders (ls/provisioner.py:442-455, 262-314). Returns the chosen tau, or NaN when no
+// candidate is feasible (InfeasibleError(gap=1.0), ls/provisioner.py:473-477).
+template <int MAXS>
+__device__ double phase_candidates(const InstanceConsts& c, const DeviceTables& tb,
+                                   const WarpSmem<MAXS>& w, int S, double tau_lo, double tau_hi,
+                                   int n_cand) {
+  const int lane = threadIdx.x & 31;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  TieBuf buf;
+  buf.init();
+  int sp = 0;
+  for (int i = lane; i < n_cand; i += 32) {
+    double tau;
+    if (i < 2) {
+      tau = (i == 0) ? tau_lo : tau_hi;
+    } else {
+      const int j = i - 2;
+      while (w.pre[sp + 1] <= j) sp++;
+      const double m = w.kmin[sp] + (double)(j - w.pre[sp]);
+      tau = et_lookup(c, tb, w.st[sp], w.ent[sp], m);
+      if (!(tau >= tau_lo && tau <= tau_hi)) continue;
+    }
+    buf.insert(candidate_cost(c, tb, w, S, tau), tau);
+  }
+  const double mf = warp_min(buf.mn);
+  if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
+  const double lim = mf + 1e-15;
+  double bt;
+  if (__any_sync(0xffffffffu, buf.overflow)) {  // rare: exact second pass with the final limit
+    bt = -inf;
+    sp = 0;
+    for (int i = lane; i < n_cand; i += 32) {
+      double tau;
+      if (i < 2) {
+        tau = (i == 0) ? tau_lo : tau_hi;
+      } else {
+        const int j = i - 2;
+        while (w.pre[sp + 1] <= j) sp++;
+        tau = et_lookup(c, tb, w.st[sp], w.ent[sp], w.kmin[sp] + (double)(j - w.pre[sp]));
+        if (!(tau >= tau_lo && tau <= tau_hi)) continue;
+      }
+      if (tau > bt && candidate_cost(c, tb, w, S, tau) <= lim) bt = tau;
+    }
+  } else {
+    bt = buf.best_tau(lim);
+  }
+  return warp_max(bt);
+}
+
+// Phase C: counts at the chosen tau, add_ps_cores (ls/provisioner.py:486-513) and the final
+// evaluate() whose monetary_cost is the score (ls/scoring.py:96-97, ls/costmodel.py:102-167).
+template <int MAXS>
+__device__ void phase_final(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
+                            int S, double tau, PlanOut& out) {
+  const int lane = threadIdx.x & 31;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  long long accel = 0, on_ps = 0;
+  double emax = 0.0;
+  for (int s = lane; s < S; s += 32) {
+    double k = (w.kmin[s] == w.kmax[s]) ? w.kmin[s] : count_at(w.st[s], tau, c.bo);
+    w.kres[s] = k;
+    const int t = w.st[s].type;
+    if (!c.is_cpu[t]) accel += (long long)k;
+    if (t == c.ps_type) on_ps += (long long)k;
+    emax = fmax(emax, et_lookup(c, tb, w.st[s], w.ent[s], k));
+  }
+  accel = warp_sum_ll(accel);
+  on_ps = warp_sum_ll(on_ps);
+  emax = warp_max(emax);
+  __syncwarp();
+  int ps = 0;
+  if (c.with_ps && accel != 0) {
+    if (c.ps_type < 0) { out.status = HPS_ST_NO_CPU_TYPE; out.cost = __longlong_as_double(0x7ff8000000000000LL); out.gap = 0; return; }
+    ps = (int)ceil(c.ps_cores_per_gpu * (double)accel - 1e-9);
+    const long long would = on_ps + ps;
+    if (would > c.quota[c.ps_type]) {
+      out.status = HPS_ST_PS_QUOTA;
+      out.gap = clamp_gap((double)(would - c.quota[c.ps_type]) / (double)c.quota[c.ps_type]);
+      out.cost = c.penalty_scale * (1.0 + pmax(0.0, out.gap));
+      return;
+    }
+  }
+  // evaluate(): overall = min_s B/et_s = B/max_s et_s (division is monotone); zero-time
+  // stages give inf (ls/costmodel.py:127-128)
+  const double overall = (emax > 0) ? c.batch / emax : inf;
+  const double exec_time = (overall > 0 && overall != inf) ? c.work / overall : 0.0;
+  double cost = 0.0;
+  if (lane == 0) {  // per_type_totals in insertion order (ls/domain.py:342-348)
+    int order[kMaxT];
+    long long tot[kMaxT];
+    int n = 0;
+    unsigned seen = 0;
+    for (int s = 0; s < S; s++) {
+      const int t = w.st[s].type;
+      if (!(seen >> t & 1u)) { seen |= 1u << t; order[n] = t; tot[n] = 0; n++; }
+      for (int j = 0; j < n; j++)
+        if (order[j] == t) { tot[j] += (long long)w.kres[s]; break; }
+    }
+    if (ps > 0) {
+      const int t = c.ps_type;
+      if (!(seen >> t & 1u)) { order[n] = t; tot[n] = 0; n++; }
+      for (int j = 0; j < n; j++)
+        if (order[j] == t) { tot[j] += ps; break; }
+    }
+    double per_second = 0.0;
+    for (int j = 0; j < n; j++) per_second += c.price_h[order[j]] / 3600.0 * (double)tot[j];
+    cost = exec_time * per_second;
+  }
+  out.cost = __shfl_sync(0xffffffffu, cost, 0);
+  out.status = HPS_ST_OK;
+  out.gap = 0.0;
+  out.ps = ps;
+}
+
+// Whole plan on one warp. Returns with out.status == kStPending when the breakpoint count
+// may exceed 4096 (the block-per-plan slow path then finishes the plan).
+template <int MAXS>
+__device__ void eval_plan_warp(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
+                               int d0, int d1, PlanOut& out) {
+  out.ps = 0;
+  out.gap = 0.0;
+  double tau_lo, tau_hi;
+  int n_cand;
+  if (!phase_stages_bisect<MAXS>(c, tb, w, d0, d1, out, tau_lo, tau_hi, n_cand)) return;
+  if (n_cand > kBpLimit) { out.status = kStPending; return; }
+  const double tau = phase_candidates<MAXS>(c, tb, w, out.S, tau_lo, tau_hi, n_cand);
+  if (tau != tau) {
+    out.status = HPS_ST_NO_CANDIDATE; out.gap = 1.0;
+    out.cost = c.penalty_scale * (1.0 + 1.0);
+    return;
+  }
+  phase_final<MAXS>(c, tb, w, out.S, tau, out);
+}
+
+}  // namespace hps

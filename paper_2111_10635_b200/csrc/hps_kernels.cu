@@ -1,0 +1,1037 @@
+// hps_kernels.cu — sm_100a kernels of the plan evaluator and the extern "C" ABI (include/hps.h).
+//
+// Kernels (SURVEY.md §2 numbering):
+//   setup      stage table (Neumaier aggregates of every (type, first, last) run), stage-0
+//              exits (min_k1 / tau_hi) and the ET table et(e, m) for m <= quota
+//   K1         score_kernel       PlanScorer.__call__ over a plan batch, one warp per plan
+//   K2         argmin_kernel      brute_force / random_search loop with a fused (cost, rank)
+//                                 argmin; plans decoded (enumeration index) or generated
+//                                 (numpy PCG64 + Lemire) in-kernel
+//   K7         slow_kernel        block per plan for the >4096-breakpoint path: sort, dedup,
+//                                 Newton/golden + subsample (ls/provisioner.py:456-470)
+//   reduce     finish_argmin      deterministic merge of per-block keys
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "hps_eval.cuh"
+
+using namespace hps;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_err(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return set_err(HPS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+constexpr int kEtCapMax = 16384;
+constexpr int kSlowBlocks = 32;
+constexpr int kSlowThreads = 256;
+
+// ------------------------------------------------------------------ plan sources
+
+struct PlanSource {
+  int32_t mode;          // 0 plans array, 1 enumeration index, 2 numpy PCG64 integers()
+  int32_t tbits;         // mode 2: log2(T)
+  const uint8_t* plans;  // mode 0
+  uint64_t begin;        // mode 1/2: first enumeration index / first random plan
+  uint64_t tpow[kMaxL];  // mode 1: T^(L-1-l)
+  // mode 2: state after (first*L/2 + 1) steps is computed per warp; A_j/C_j advance it by j
+  uint64_t s0_hi, s0_lo, inc_hi, inc_lo;
+  uint64_t jA_hi[33], jA_lo[33], jC_hi[33], jC_lo[33];
+};
+
+__host__ __device__ __forceinline__ u128 mk(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
+
+// digits of plan number p (relative to src.begin) for this lane: d0 = layer lane, d1 = lane+32
+__device__ __forceinline__ void load_digits(const InstanceConsts& c, const PlanSource& src,
+                                            uint64_t p, int& d0, int& d1, u128& rank) {
+  const int lane = threadIdx.x & 31;
+  const int L = c.L;
+  d0 = 0;
+  d1 = 0;
+  if (src.mode == 0) {
+    const uint8_t* row = src.plans + p * (uint64_t)L;
+    if (lane < L) d0 = row[lane];
+    if (lane + 32 < L) d1 = row[lane + 32];
+    rank = 0;
+    if (src.tbits > 0) {  // argmin over an explicit batch: packed lexicographic rank
+      u128 part = 0;
+      for (int slot = 0; slot < 2; slot++) {
+        const int l = lane + 32 * slot;
+        if (l < L) part |= (u128)((slot ? d1 : d0) & ((1 << src.tbits) - 1)) << ((L - 1 - l) * src.tbits);
+      }
+      uint64_t hi = (uint64_t)(part >> 64), lo = (uint64_t)part;
+      for (int o = 16; o; o >>= 1) {
+        hi |= __shfl_xor_sync(0xffffffffu, hi, o);
+        lo |= __shfl_xor_sync(0xffffffffu, lo, o);
+      }
+      rank = mk(hi, lo);
+    }
+  } else if (src.mode == 1) {
+    const uint64_t idx = src.begin + p;
+    if (lane < L) d0 = (int)((idx / src.tpow[lane]) % (uint64_t)c.T);
+    if (lane + 32 < L) d1 = (int)((idx / src.tpow[lane + 32]) % (uint64_t)c.T);
+    rank = idx;
+  } else {
+    const uint64_t g = src.begin + p;
+    if (c.T > 1) {
+      // 32-bit half h = g*L + l of the PCG64 stream: draw h>>1, low half first
+      const u128 h0 = (u128)g * (u128)L;
+      const u128 base = h0 >> 1;
+      u128 sb = 0;
+      if (lane == 0) sb = pcg_advance(mk(src.s0_hi, src.s0_lo), mk(src.inc_hi, src.inc_lo), base + 1);
+      uint64_t sb_hi = __shfl_sync(0xffffffffu, (uint64_t)(sb >> 64), 0);
+      uint64_t sb_lo = __shfl_sync(0xffffffffu, (uint64_t)sb, 0);
+      sb = mk(sb_hi, sb_lo);
+      for (int slot = 0; slot < 2; slot++) {
+        const int l = lane + 32 * slot;
+        if (l < L) {
+          const u128 h = h0 + (u128)l;
+          const int j = (int)((h >> 1) - base);
+          const u128 st = mk(src.jA_hi[j], src.jA_lo[j]) * sb + mk(src.jC_hi[j], src.jC_lo[j]);
+          const uint64_t v = pcg_output(st);
+          const uint32_t u = (h & 1) ? (uint32_t)(v >> 32) : (uint32_t)v;
+          const int dg = (int)(u >> (32 - src.tbits));
+          if (slot == 0) d0 = dg; else d1 = dg;
+        }
+      }
+    }
+    // lexicographic rank: base-T digits, layer 0 most significant (T = 2^tbits)
+    u128 part = 0;
+    for (int slot = 0; slot < 2; slot++) {
+      const int l = lane + 32 * slot;
+      if (l < L) part |= (u128)(slot ? d1 : d0) << ((L - 1 - l) * src.tbits);
+    }
+    uint64_t hi = (uint64_t)(part >> 64), lo = (uint64_t)part;
+    for (int o = 16; o; o >>= 1) {
+      hi |= __shfl_xor_sync(0xffffffffu, hi, o);
+      lo |= __shfl_xor_sync(0xffffffffu, lo, o);
+    }
+    rank = mk(hi, lo);
+  }
+}
+
+// ------------------------------------------------------------------ argmin keys
+
+struct Key {
+  double cost;  // +inf = nothing
+  uint64_t hi, lo;
+  uint32_t status;
+};
+
+__device__ __forceinline__ bool key_less(const Key& a, const Key& b) {
+  if (a.cost != b.cost) return a.cost < b.cost;
+  if (a.hi != b.hi) return a.hi < b.hi;
+  return a.lo < b.lo;
+}
+
+struct KeyPart {  // per-block partial of an argmin launch
+  Key best;
+  unsigned long long evaluated, feasible;
+  uint32_t flags;  // bit0: a plan needed NO_CPU_TYPE, bit1: INVALID
+};
+
+struct Outputs {  // mode 0 per-plan outputs (HpsPlanResults)
+  double* cost;
+  uint8_t* status;
+  double* gap;
+  int32_t* ps;
+  int32_t* num_stages;
+  int32_t* k;
+};
+
+struct Pending {
+  unsigned long long* list;  // plan numbers that need the slow path
+  unsigned int* count;
+  unsigned int cap;
+};
+
+template <int MAXS>
+__device__ __forceinline__ void write_plan(const InstanceConsts& c, const WarpSmem<MAXS>& w,
+                                           const Outputs& o, uint64_t p, const PlanOut& r) {
+  const int lane = threadIdx.x & 31;
+  const bool ok = (r.status & 0x7f) == HPS_ST_OK;
+  if (lane == 0) {
+    o.cost[p] = r.cost;
+    o.status[p] = (uint8_t)r.status;
+    if (o.gap) o.gap[p] = r.gap;
+    if (o.ps) o.ps[p] = ok ? r.ps : 0;
+    if (o.num_stages) o.num_stages[p] = r.S;
+  }
+  if (o.k) {
+    for (int s = lane; s < c.L; s += 32)
+      o.k[p * (uint64_t)c.L + s] = (ok && s < r.S) ? (int32_t)w.kres[s] : 0;
+  }
+}
+
+// ------------------------------------------------------------------ K1 / K2
+
+template <int MAXS, int WARPS, bool ARGMIN>
+__global__ void __launch_bounds__(WARPS * 32)
+eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, uint64_t n,
+            Outputs o, Pending pend, int feasible_only, KeyPart* parts) {
+  __shared__ WarpSmem<MAXS> sm[WARPS];
+  __shared__ KeyPart bparts[WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem<MAXS>& w = sm[warp];
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
+  Key best;
+  best.cost = __longlong_as_double(0x7ff0000000000000LL);
+  best.hi = best.lo = ~0ull;
+  best.status = 0;
+  unsigned long long feas = 0;
+  uint32_t flags = 0;
+  for (uint64_t p = gw; p < n; p += nw) {
+    int d0, d1;
+    u128 rank;
+    load_digits(c, src, p, d0, d1, rank);
+    PlanOut r;
+    eval_plan_warp<MAXS>(c, tb, w, d0, d1, r);
+    if (r.status == kStPending) {
+      if (lane == 0) {
+        unsigned int at = atomicAdd(pend.count, 1u);
+        if (at < pend.cap) pend.list[at] = p;
+      }
+    } else if (!ARGMIN) {
+      write_plan<MAXS>(c, w, o, p, r);
+    } else {
+      const int code = r.status & 0x7f;
+      if (code == HPS_ST_OK) feas++;
+      if (code == HPS_ST_NO_CPU_TYPE) flags |= 1u;
+      if (code == HPS_ST_INVALID) flags |= 2u;
+      const bool take = feasible_only ? (code == HPS_ST_OK) : (code != HPS_ST_NO_CPU_TYPE && code != HPS_ST_INVALID);
+      if (take) {
+        Key k{r.cost, (uint64_t)(rank >> 64), (uint64_t)rank, (uint32_t)r.status};
+        if (key_less(k, best)) best = k;
+      }
+    }
+    __syncwarp();
+  }
+  if (ARGMIN) {
+    if (lane == 0) bparts[warp] = KeyPart{best, 0ull, feas, flags};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      KeyPart acc = bparts[0];
+      for (int i = 1; i < WARPS; i++) {
+        if (key_less(bparts[i].best, acc.best)) acc.best = bparts[i].best;
+        acc.feasible += bparts[i].feasible;
+        acc.flags |= bparts[i].flags;
+      }
+      parts[blockIdx.x] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K7 slow path
+
+__device__ double real_cost_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double tau) {
+  // _CostModel.real_cost (ls/provisioner.py:230-249)
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double ks[kMaxL];
+  for (int s = 0; s < S; s++) {
+    double r, g;
+    if (!floor_count(w.st[s], tau, c.bo, r, g)) return inf;
+    ks[s] = pmax(1.0, r);
+  }
+  double et = stage_et(w.st[0], ks[0]);
+  for (int s = 1; s < S; s++) et = pmax(et, stage_et(w.st[s], ks[s]));
+  if (et <= 0) return 0.0;
+  const double thr = c.batch / et;
+  if (!(thr > c.limit)) return inf;
+  PySum ps;
+  for (int s = 0; s < S; s++) ps.add(c.price_s[w.st[s].type] * ks[s]);
+  return c.work / thr * ps.result();
+}
+
+__device__ bool newton_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double lo, double hi,
+                           double& xo) {  // _newton_minimize (ls/provisioner.py:317-345)
+  const double h = pmax(c.fd_step * (hi - lo), 1e-12);
+  double x = pmin(hi - h, lo + pmax(h, (hi - lo) * 0.25));
+  if (x <= lo + h) return false;
+  for (int it = 0; it < c.newton_max_iters; it++) {
+    const double fm = real_cost_dev(c, w, S, x - h), f0 = real_cost_dev(c, w, S, x),
+                 fp = real_cost_dev(c, w, S, x + h);
+    if (!(isfinite(fm) && isfinite(f0) && isfinite(fp))) return false;
+    const double d1 = (fp - fm) / (2.0 * h);
+    const double d2 = (fp - 2.0 * f0 + fm) / (h * h);
+    if (fabs(d2) < 1e-18) return false;
+    const double step = d1 / d2;
+    const double xn = x - step;
+    if (!isfinite(xn) || xn < lo || xn > hi) return false;
+    if (fabs(xn - x) < c.newton_tol * pmax(1.0, fabs(x))) {
+      if (real_cost_dev(c, w, S, xn) <= f0 + 1e-12) { xo = xn; return true; }
+      return false;
+    }
+    x = xn;
+  }
+  return false;
+}
+
+__device__ double golden_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double lo, double hi) {
+  // _golden_minimize (ls/provisioner.py:348-371)
+  if (hi <= lo) return lo;
+  const int n = 17;
+  double xs[17], vals[17];
+  for (int i = 0; i < n; i++) {
+    xs[i] = lo + (hi - lo) * (double)i / (double)(n - 1);
+    vals[i] = real_cost_dev(c, w, S, xs[i]);
+  }
+  int best = 0;
+  for (int i = 1; i < n; i++)
+    if (vals[i] < vals[best]) best = i;
+  double a = xs[best > 0 ? best - 1 : 0], b = xs[best + 1 < n ? best + 1 : n - 1];
+  const double inv_phi = (sqrt(5.0) - 1.0) / 2.0;
+  double cc = b - inv_phi * (b - a), dd = a + inv_phi * (b - a);
+  double fc = real_cost_dev(c, w, S, cc), fd = real_cost_dev(c, w, S, dd);
+  for (int it = 0; it < 60; it++) {
+    if (fc <= fd) {
+      b = dd; dd = cc; fd = fc;
+      cc = b - inv_phi * (b - a);
+      fc = real_cost_dev(c, w, S, cc);
+    } else {
+      a = cc; cc = dd; fc = fd;
+      dd = a + inv_phi * (b - a);
+      fd = real_cost_dev(c, w, S, dd);
+    }
+  }
+  return (a + b) / 2.0;
+}
+
+// block-wide exclusive scan helper over per-thread counts (kSlowThreads threads)
+__device__ unsigned block_excl_scan(unsigned v, unsigned* tmp, unsigned& total) {
+  tmp[threadIdx.x] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned acc = 0;
+    for (int i = 0; i < kSlowThreads; i++) { unsigned t = tmp[i]; tmp[i] = acc; acc += t; }
+    tmp[kSlowThreads] = acc;
+  }
+  __syncthreads();
+  unsigned r = tmp[threadIdx.x];
+  total = tmp[kSlowThreads];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kSlowThreads)
+slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, Outputs o,
+            Pending pend, int argmin_mode, int feasible_only, KeyPart* slow_parts,
+            double* scratch, size_t per_block) {
+  __shared__ WarpSmem<64> w;
+  __shared__ unsigned scan_tmp[kSlowThreads + 1];
+  __shared__ double red_d[kSlowThreads];
+  __shared__ unsigned long long red_i[kSlowThreads];
+  __shared__ double s_tau_lo, s_tau_hi, s_tau_star;
+  __shared__ int s_ncand, s_S, s_done;
+  __shared__ PlanOut s_out;
+  __shared__ u128 s_rank;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* raw = scratch + (size_t)blockIdx.x * per_block;  // [per_block/2] sort buffer
+  double* cand = raw + per_block / 2;                       // distinct / kept candidates
+  const unsigned total = min(*pend.count, pend.cap);
+  for (unsigned item = blockIdx.x; item < total; item += gridDim.x) {
+    const uint64_t p = pend.list[item];
+    if (warp == 0) {
+      int d0, d1;
+      u128 rank;
+      load_digits(c, src, p, d0, d1, rank);
+      PlanOut r;
+      r.ps = 0; r.gap = 0.0;
+      double tlo = 0, thi = 0;
+      int ncand = 0;
+      const bool go = phase_stages_bisect<64>(c, tb, w, d0, d1, r, tlo, thi, ncand);
+      if (lane == 0) {
+        s_out = r; s_tau_lo = tlo; s_tau_hi = thi; s_ncand = ncand; s_S = r.S; s_done = go ? 0 : 1;
+        s_rank = rank;
+      }
+    }
+    __syncthreads();
+    if (!s_done) {
+      const int S = s_S;
+      const double tau_lo = s_tau_lo, tau_hi = s_tau_hi;
+      const int nraw = s_ncand;
+      int npow = 1;
+      while (npow < nraw) npow <<= 1;
+      // raw candidates (class leaders' breakpoints + tau_lo/tau_hi), out-of-range -> +inf
+      for (int i = tid; i < npow; i += kSlowThreads) {
+        double v = __longlong_as_double(0x7ff0000000000000LL);
+        if (i == 0) v = tau_lo;
+        else if (i == 1) v = tau_hi;
+        else if (i < nraw) {
+          const int j = i - 2;
+          int lo = 0, hi = S;  // find stage: pre[lo] <= j < pre[lo+1]
+          while (hi - lo > 1) { int mid = (lo + hi) / 2; if (w.pre[mid] <= j) lo = mid; else hi = mid; }
+          while (w.pre[lo + 1] <= j) lo++;
+          v = et_lookup(c, tb, w.st[lo], w.ent[lo], w.kmin[lo] + (double)(j - w.pre[lo]));
+          if (!(v >= tau_lo && v <= tau_hi)) v = __longlong_as_double(0x7ff0000000000000LL);
+        }
+        raw[i] = v;
+      }
+      __syncthreads();
+      for (int k = 2; k <= npow; k <<= 1)  // bitonic sort ascending
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = tid; i < npow; i += kSlowThreads) {
+            const int l = i ^ j;
+            if (l > i) {
+              const double a = raw[i], b = raw[l];
+              const bool up = (i & k) == 0;
+              if (up ? (a > b) : (a < b)) { raw[i] = b; raw[l] = a; }
+            }
+          }
+          __syncthreads();
+        }
+      // distinct finite values -> cand (chunked compaction)
+      const int chunk = (npow + kSlowThreads - 1) / kSlowThreads;
+      const int b0 = min(npow, tid * chunk), b1 = min(npow, b0 + chunk);
+      unsigned cnt = 0;
+      for (int i = b0; i < b1; i++)
+        if (raw[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || raw[i] != raw[i - 1])) cnt++;
+      unsigned nc;
+      unsigned at = block_excl_scan(cnt, scan_tmp, nc);
+      for (int i = b0; i < b1; i++)
+        if (raw[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || raw[i] != raw[i - 1])) cand[at++] = raw[i];
+      __syncthreads();
+      bool ovf = false;
+      if (nc > (unsigned)kBpLimit) {  // ls/provisioner.py:456-470
+        ovf = true;
+        if (tid == 0) {
+          double ts;
+          if (!newton_dev(c, w, S, tau_lo, tau_hi, ts)) ts = golden_dev(c, w, S, tau_lo, tau_hi);
+          s_tau_star = ts;
+        }
+        __syncthreads();
+        const double ts = s_tau_star;
+        // centre = first index of the minimum |cand[i] - tau_star|
+        double bd = __longlong_as_double(0x7ff0000000000000LL);
+        unsigned long long bi = ~0ull;
+        for (unsigned i = tid; i < nc; i += kSlowThreads) {
+          double dd = fabs(cand[i] - ts);
+          if (dd < bd || (dd == bd && i < bi)) { bd = dd; bi = i; }
+        }
+        red_d[tid] = bd; red_i[tid] = bi;
+        __syncthreads();
+        if (tid == 0) {
+          for (int i = 1; i < kSlowThreads; i++)
+            if (red_d[i] < red_d[0] || (red_d[i] == red_d[0] && red_i[i] < red_i[0])) { red_d[0] = red_d[i]; red_i[0] = red_i[i]; }
+        }
+        __syncthreads();
+        const unsigned long long centre = red_i[0];
+        const double step = (double)nc / (double)(kBpLimit / 2);
+        // kept indices: {0, nc-1} U {int(i*step)} U [centre-256, centre+256)
+        uint8_t* keep = reinterpret_cast<uint8_t*>(raw);  // raw is free now
+        for (unsigned i = tid; i < nc; i += kSlowThreads) keep[i] = 0;
+        __syncthreads();
+        if (tid == 0) { keep[0] = 1; keep[nc - 1] = 1; }
+        for (int i = tid; i < kBpLimit / 2; i += kSlowThreads) keep[(unsigned long long)((double)i * step)] = 1;
+        const long long lo_i = (long long)centre >= 256 ? (long long)centre - 256 : 0;
+        const long long hi_i = (long long)centre + 256 < (long long)nc ? (long long)centre + 256 : (long long)nc;
+        for (long long i = lo_i + tid; i < hi_i; i += kSlowThreads) keep[i] = 1;
+        __syncthreads();
+        const int ch2 = (nc + kSlowThreads - 1) / kSlowThreads;
+        const unsigned e0 = min(nc, (unsigned)(tid * ch2)), e1 = min(nc, e0 + ch2);
+        unsigned kc = 0;
+        for (unsigned i = e0; i < e1; i++) kc += keep[i];
+        unsigned nk;
+        unsigned pos = block_excl_scan(kc, scan_tmp, nk);
+        double* kept = reinterpret_cast<double*>(raw) + (per_block / 4);  // upper half of raw
+        for (unsigned i = e0; i < e1; i++)
+          if (keep[i]) kept[pos++] = cand[i];
+        __syncthreads();
+        for (unsigned i = tid; i < nk; i += kSlowThreads) cand[i] = kept[i];
+        __syncthreads();
+        nc = nk;
+      }
+      // _best_candidate over the explicit list, all threads
+      TieBuf buf;
+      buf.init();
+      for (unsigned i = tid; i < nc; i += kSlowThreads) buf.insert(candidate_cost<64>(c, tb, w, S, cand[i]), cand[i]);
+      red_d[tid] = buf.mn;
+      __syncthreads();
+      if (tid == 0) for (int i = 1; i < kSlowThreads; i++) red_d[0] = fmin(red_d[0], red_d[i]);
+      __syncthreads();
+      const double mf = red_d[0];
+      __syncthreads();
+      const bool any_ovf = __syncthreads_or(buf.overflow);
+      double bt = -__longlong_as_double(0x7ff0000000000000LL);
+      if (mf < __longlong_as_double(0x7ff0000000000000LL)) {
+        const double lim = mf + 1e-15;
+        if (any_ovf) {
+          for (unsigned i = tid; i < nc; i += kSlowThreads)
+            if (cand[i] > bt && candidate_cost<64>(c, tb, w, S, cand[i]) <= lim) bt = cand[i];
+        } else {
+          bt = buf.best_tau(lim);
+        }
+      }
+      red_d[tid] = bt;
+      __syncthreads();
+      if (tid == 0) for (int i = 1; i < kSlowThreads; i++) red_d[0] = fmax(red_d[0], red_d[i]);
+      __syncthreads();
+      const double tau = red_d[0];
+      if (warp == 0) {
+        PlanOut r = s_out;
+        if (!(mf < __longlong_as_double(0x7ff0000000000000LL))) {
+          r.status = HPS_ST_NO_CANDIDATE; r.gap = 1.0; r.cost = c.penalty_scale * 2.0;
+        } else {
+          phase_final<64>(c, tb, w, S, tau, r);
+        }
+        if (ovf) r.status |= HPS_ST_OVERFLOW_FLAG;
+        if (lane == 0) s_out = r;
+      }
+      __syncthreads();
+    }
+    // emit
+    if (warp == 0) {
+      PlanOut r = s_out;
+      if (!argmin_mode) {
+        write_plan<64>(c, w, o, p, r);
+      } else if (lane == 0) {
+        const int code = r.status & 0x7f;
+        KeyPart kp;
+        kp.best.cost = __longlong_as_double(0x7ff0000000000000LL);
+        kp.best.hi = kp.best.lo = ~0ull;
+        kp.best.status = 0;
+        kp.evaluated = 0;
+        kp.feasible = (code == HPS_ST_OK);
+        kp.flags = (code == HPS_ST_NO_CPU_TYPE ? 1u : 0u) | (code == HPS_ST_INVALID ? 2u : 0u);
+        const bool take = feasible_only ? (code == HPS_ST_OK) : (code != HPS_ST_NO_CPU_TYPE && code != HPS_ST_INVALID);
+        if (take) kp.best = Key{r.cost, (uint64_t)(s_rank >> 64), (uint64_t)s_rank, (uint32_t)r.status};
+        slow_parts[item] = kp;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void finish_argmin(const KeyPart* parts, int nparts, const KeyPart* slow_parts,
+                              const unsigned int* slow_count, unsigned int slow_cap,
+                              uint64_t evaluated, HpsArgmin* out) {
+  __shared__ KeyPart red[256];
+  KeyPart acc;
+  acc.best.cost = __longlong_as_double(0x7ff0000000000000LL);
+  acc.best.hi = acc.best.lo = ~0ull;
+  acc.best.status = 0;
+  acc.feasible = 0;
+  acc.flags = 0;
+  const unsigned ns = min(*slow_count, slow_cap);
+  for (int i = threadIdx.x; i < nparts + (int)ns; i += blockDim.x) {
+    const KeyPart& k = (i < nparts) ? parts[i] : slow_parts[i - nparts];
+    if (key_less(k.best, acc.best)) acc.best = k.best;
+    acc.feasible += k.feasible;
+    acc.flags |= k.flags;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)blockDim.x; i++) {
+      if (key_less(red[i].best, acc.best)) acc.best = red[i].best;
+      acc.feasible += red[i].feasible;
+      acc.flags |= red[i].flags;
+    }
+    out->cost = acc.best.cost;
+    out->rank_hi = acc.best.hi;
+    out->rank_lo = acc.best.lo;
+    out->evaluated = evaluated;
+    out->feasible = acc.feasible;
+    out->status = acc.best.status;
+    out->flags = acc.flags;
+  }
+}
+
+// ------------------------------------------------------------------ setup kernels
+
+struct RawTables {
+  const double *oct, *odt, *alpha, *beta;  // [T][L]
+};
+
+__global__ void stage_table_kernel(const InstanceConsts c, RawTables raw, StageEntry* out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= c.T * c.P) return;
+  const int t = idx / c.P, pe = idx % c.P;
+  int last = 0;
+  while ((last + 1) * (last + 2) / 2 <= pe) last++;
+  const int first = pe - last * (last + 1) / 2;
+  const int L = c.L;
+  // build_stages aggregates (ls/domain.py:298-325)
+  PySum so, sw, sa, sd, sv, sb;
+  bool valid = true;
+  for (int l = first; l <= last; l++) {
+    const double o = raw.oct[t * L + l], d = raw.odt[t * L + l], a = raw.alpha[t * L + l], b = raw.beta[t * L + l];
+    if (o != o || d != d || a != a || b != b) valid = false;
+    so.add(o);
+    sw.add(o * a);
+    sa.add(a);
+    sd.add(d);
+    sv.add(d * b);
+    sb.add(b);
+  }
+  const int n = last - first + 1;
+  StageEntry e;
+  e.oct = so.result();
+  e.alpha = (e.oct > 0) ? sw.result() / e.oct : sa.result() / (double)n;
+  const double odt_sum = sd.result();
+  e.beta = (odt_sum > 0) ? sv.result() / odt_sum : sb.result() / (double)n;
+  e.odt = raw.odt[t * L + last];
+  e.c_oct = e.oct / c.bo;
+  e.c_odt = e.odt / c.bo;
+  e.oma = 1.0 - e.alpha;
+  e.omb = 1.0 - e.beta;
+  e.serial = pmax(e.c_oct * e.oma, e.c_odt * e.omb);
+  e.valid = valid ? 1 : 0;
+  e.type = t;
+  out[idx] = e;
+}
+
+__global__ void stage0_kernel(const InstanceConsts c, const StageEntry* st, Stage0Info* out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= c.T * c.L) return;
+  const int t = idx / c.L, last = idx % c.L;
+  const StageEntry& s = st[entry_index(c.P, t, 0, last)];
+  Stage0Info r;
+  r.status = HPS_ST_OK;
+  r.gap = 0.0;
+  r.pad = 0;
+  // min_k1 (ls/provisioner.py:80-104)
+  const double budget = c.limit * c.bo;
+  double b[2] = {0.0, 0.0};
+  const double works[2] = {s.oct, s.odt}, fr[2] = {s.alpha, s.beta};
+  for (int i = 0; i < 2 && r.status == HPS_ST_OK; i++) {
+    if (works[i] == 0) continue;
+    const double denom = budget - (1.0 - fr[i]) * works[i];
+    if (denom <= 0) {
+      r.status = HPS_ST_MIN_K1;
+      r.gap = clamp_gap(((1.0 - fr[i]) * works[i] - budget) / budget);
+    } else {
+      b[i] = fr[i] * works[i] / denom;
+    }
+  }
+  double tau_hi = c.tau_limit;
+  if (r.status == HPS_ST_OK) {
+    const double k1 = pmax(b[0], b[1]);
+    if (k1 > 1.0) tau_hi = pmin(tau_hi, stage_et(s, k1));
+  }
+  r.tau_hi = tau_hi;
+  out[idx] = r;
+}
+
+__global__ void et_table_kernel(const InstanceConsts c, const StageEntry* st, double* et, int t,
+                                int64_t count) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  const int cap = c.et_cap[t];
+  const int64_t pe = idx / cap;
+  const double m = (double)(idx % cap + 1);
+  et[c.et_off[t] + idx] = stage_et(st[t * c.P + pe], m);
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+
+struct HpsInstance {
+  InstanceConsts c;
+  DeviceTables tb;
+  StageEntry* d_stages = nullptr;
+  Stage0Info* d_stage0 = nullptr;
+  double* d_et = nullptr;
+  int32_t* d_cls = nullptr;
+  std::vector<StageEntry> h_stages;
+  int sm_count = 148;
+};
+
+namespace {
+
+template <int MAXS, int WARPS, bool ARGMIN>
+int launch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
+                int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
+  eval_kernel<MAXS, WARPS, ARGMIN><<<grid, WARPS * 32, 0, st>>>(in->c, in->tb, src, n, o, pend,
+                                                                feasible_only, parts);
+  CUDA_TRY(cudaGetLastError());
+  return HPS_OK;
+}
+
+template <bool ARGMIN>
+int dispatch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
+                  int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
+  if (in->c.L <= 16) return launch_eval<16, 8, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (in->c.L <= 32) return launch_eval<32, 8, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  return launch_eval<64, 4, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
+}
+
+int grid_for(HpsInstance* in, uint64_t n_plans) {
+  const int warps = (in->c.L <= 32) ? 8 : 4;
+  uint64_t blocks = (n_plans + warps - 1) / warps;
+  uint64_t cap = (uint64_t)in->sm_count * 8;
+  return (int)std::max<uint64_t>(1, std::min(blocks, cap));
+}
+
+size_t slow_per_block(const HpsInstance* in) {
+  size_t nraw = (size_t)in->c.L * (kBpLimit + 1) + 2;
+  size_t npow = 1;
+  while (npow < nraw) npow <<= 1;
+  return 2 * npow;  // doubles: sort buffer + candidate buffer
+}
+
+int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending pend, int argmin_mode,
+             int feasible_only, KeyPart* slow_parts, cudaStream_t st) {
+  const size_t per_block = slow_per_block(in);
+  double* scratch = nullptr;
+  CUDA_TRY(cudaMallocAsync(&scratch, per_block * kSlowBlocks * sizeof(double), st));
+  slow_kernel<<<kSlowBlocks, kSlowThreads, 0, st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
+                                                    slow_parts, scratch, per_block);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(scratch, st));
+  return HPS_OK;
+}
+
+void fill_random_source(HpsInstance* in, const HpsPcg64* g, uint64_t first, PlanSource& src) {
+  src.mode = 2;
+  src.begin = first;
+  int b = 0;
+  while ((1 << b) < in->c.T) b++;
+  src.tbits = b;
+  src.s0_hi = g->state_hi; src.s0_lo = g->state_lo;
+  src.inc_hi = g->inc_hi; src.inc_lo = g->inc_lo;
+  const u128 inc = mk(g->inc_hi, g->inc_lo), M = pcg_mult();
+  u128 A = 1, Cc = 0;
+  for (int j = 0; j <= 32; j++) {
+    src.jA_hi[j] = (uint64_t)(A >> 64); src.jA_lo[j] = (uint64_t)A;
+    src.jC_hi[j] = (uint64_t)(Cc >> 64); src.jC_lo[j] = (uint64_t)Cc;
+    A = M * A;
+    Cc = M * Cc + inc;
+  }
+}
+
+const uint64_t kSlowCap = 1u << 20;
+
+struct ArgminScratch {
+  KeyPart* parts;
+  KeyPart* slow_parts;
+  unsigned long long* list;
+  unsigned int* count;
+};
+
+int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_only, HpsArgmin* d_best,
+                  cudaStream_t st) {
+  const int grid = grid_for(in, n);
+  const unsigned cap = (unsigned)std::min<uint64_t>(kSlowCap, std::max<uint64_t>(n, 1));
+  char* buf = nullptr;
+  const size_t bytes = sizeof(KeyPart) * (grid + cap) + sizeof(unsigned long long) * cap + 64;
+  CUDA_TRY(cudaMallocAsync(&buf, bytes, st));
+  KeyPart* parts = reinterpret_cast<KeyPart*>(buf);
+  KeyPart* slow_parts = parts + grid;
+  unsigned long long* list = reinterpret_cast<unsigned long long*>(slow_parts + cap);
+  unsigned int* count = reinterpret_cast<unsigned int*>(list + cap);
+  CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
+  Pending pend{list, count, cap};
+  Outputs o{};
+  int rc = dispatch_eval<true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (rc) return rc;
+  rc = run_slow(in, src, o, pend, 1, feasible_only, slow_parts, st);
+  if (rc) return rc;
+  finish_argmin<<<1, 256, 0, st>>>(parts, grid, slow_parts, count, cap, n, d_best);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(buf, st));
+  return HPS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hps_abi_version(void) { return HPS_ABI_VERSION; }
+
+const char* hps_error_string(int code) {
+  switch (code) {
+    case HPS_OK: return "ok";
+    case HPS_E_INVALID_ARG: return "invalid argument";
+    case HPS_E_PLAN: return "plan does not fit the model graph or catalog";
+    case HPS_E_CONFIG: return "configuration not supported";
+    case HPS_E_CUDA: return "CUDA runtime failure";
+    case HPS_E_NO_CPU_TYPE: return "catalog has no CPU-capable resource type";
+    case HPS_E_NUMERIC: return "non-finite values";
+    default: return "unknown error";
+  }
+}
+
+const char* hps_last_error(void) { return g_last_error.c_str(); }
+
+int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
+  if (!d || !out) return set_err(HPS_E_INVALID_ARG, "null argument");
+  const int L = d->num_layers, T = d->num_types;
+  if (L < 1 || L > kMaxL || T < 1 || T > kMaxT) return set_err(HPS_E_CONFIG, "L or T out of range");
+  if (!(d->throughput_limit > 0) || d->profile_batch_size < 1 || d->batch_size < 1)
+    return set_err(HPS_E_INVALID_ARG, "bad job parameters");
+  int dev = 0, ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (ndev < 1) return set_err(HPS_E_CUDA, "no CUDA device");
+  CUDA_TRY(cudaGetDevice(&dev));
+  auto* in = new HpsInstance();
+  cudaDeviceGetAttribute(&in->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  InstanceConsts& c = in->c;
+  memset(&c, 0, sizeof(c));
+  c.L = L; c.T = T; c.P = L * (L + 1) / 2;
+  c.with_ps = d->with_ps;
+  c.newton_max_iters = d->newton_max_iters;
+  c.bo = (double)d->profile_batch_size;
+  c.batch = (double)d->batch_size;
+  c.work = (double)(d->epochs * d->total_samples);
+  c.limit = d->throughput_limit;
+  c.ps_cores_per_gpu = d->ps_cores_per_gpu;
+  c.newton_tol = d->newton_tol;
+  c.fd_step = d->fd_step;
+  c.tau_limit = c.batch / c.limit;
+  double mx = d->price_per_hour[0];
+  c.ps_type = -1;
+  for (int t = 0; t < T; t++) {
+    if (d->price_per_hour[t] > mx) mx = d->price_per_hour[t];
+    c.price_h[t] = d->price_per_hour[t];
+    c.price_s[t] = d->price_per_hour[t] / 3600.0;
+    c.quota[t] = d->quota[t];
+    c.is_cpu[t] = d->is_cpu[t] ? 1 : 0;
+    if (c.is_cpu[t] && (c.ps_type < 0 || d->price_per_hour[t] < d->price_per_hour[c.ps_type])) c.ps_type = t;
+  }
+  c.penalty_scale = 1e6 * mx;
+  int64_t off = 0;
+  for (int t = 0; t < T; t++) {
+    c.et_cap[t] = (int32_t)std::max<int64_t>(1, std::min<int64_t>(d->quota[t], kEtCapMax));
+    c.et_off[t] = off;
+    off += (int64_t)c.P * c.et_cap[t];
+  }
+  // raw tables -> device
+  const size_t tl = (size_t)T * L * sizeof(double);
+  double* d_raw = nullptr;
+  CUDA_TRY(cudaMalloc(&d_raw, 4 * tl));
+  CUDA_TRY(cudaMemcpy(d_raw, d->oct, tl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy((char*)d_raw + tl, d->odt, tl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy((char*)d_raw + 2 * tl, d->alpha, tl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy((char*)d_raw + 3 * tl, d->beta, tl, cudaMemcpyHostToDevice));
+  RawTables raw{d_raw, d_raw + T * L, d_raw + 2 * T * L, d_raw + 3 * T * L};
+  const int ne = T * c.P;
+  CUDA_TRY(cudaMalloc(&in->d_stages, sizeof(StageEntry) * ne));
+  CUDA_TRY(cudaMalloc(&in->d_stage0, sizeof(Stage0Info) * T * L));
+  CUDA_TRY(cudaMalloc(&in->d_et, sizeof(double) * off));
+  CUDA_TRY(cudaMalloc(&in->d_cls, sizeof(int32_t) * ne));
+  stage_table_kernel<<<(ne + 127) / 128, 128>>>(c, raw, in->d_stages);
+  CUDA_TRY(cudaGetLastError());
+  stage0_kernel<<<(T * L + 127) / 128, 128>>>(c, in->d_stages, in->d_stage0);
+  CUDA_TRY(cudaGetLastError());
+  for (int t = 0; t < T; t++) {
+    const int64_t cnt = (int64_t)c.P * c.et_cap[t];
+    et_table_kernel<<<(unsigned)((cnt + 255) / 256), 256>>>(c, in->d_stages, in->d_et, t, cnt);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaFree(d_raw));
+  // ET-equivalence classes: group entries with bitwise-equal (oct, odt, alpha, beta)
+  in->h_stages.resize(ne);
+  CUDA_TRY(cudaMemcpy(in->h_stages.data(), in->d_stages, sizeof(StageEntry) * ne, cudaMemcpyDeviceToHost));
+  std::map<std::tuple<uint64_t, uint64_t, uint64_t, uint64_t>, int> ids;
+  std::vector<int32_t> cls(ne);
+  for (int e = 0; e < ne; e++) {
+    const StageEntry& s = in->h_stages[e];
+    uint64_t k[4];
+    memcpy(&k[0], &s.oct, 8); memcpy(&k[1], &s.odt, 8); memcpy(&k[2], &s.alpha, 8); memcpy(&k[3], &s.beta, 8);
+    auto key = std::make_tuple(k[0], k[1], k[2], k[3]);
+    auto it = ids.find(key);
+    if (it == ids.end()) it = ids.emplace(key, (int)ids.size()).first;
+    cls[e] = it->second;
+  }
+  CUDA_TRY(cudaMemcpy(in->d_cls, cls.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
+  in->tb = DeviceTables{in->d_stages, in->d_stage0, in->d_et, in->d_cls};
+  *out = in;
+  return HPS_OK;
+}
+
+int hps_instance_destroy(HpsInstance* in) {
+  if (!in) return HPS_OK;
+  cudaFree(in->d_stages);
+  cudaFree(in->d_stage0);
+  cudaFree(in->d_et);
+  cudaFree(in->d_cls);
+  delete in;
+  return HPS_OK;
+}
+
+int hps_stage_table(HpsInstance* in, int32_t t, int32_t first, int32_t last, double* out4) {
+  if (!in || !out4) return set_err(HPS_E_INVALID_ARG, "null argument");
+  if (t < 0 || t >= in->c.T || first < 0 || last < first || last >= in->c.L)
+    return set_err(HPS_E_INVALID_ARG, "stage range out of bounds");
+  const StageEntry& s = in->h_stages[entry_index(in->c.P, t, first, last)];
+  if (!s.valid) return set_err(HPS_E_PLAN, "layer profiles do not cover the type");
+  out4[0] = s.oct; out4[1] = s.odt; out4[2] = s.alpha; out4[3] = s.beta;
+  return HPS_OK;
+}
+
+int hps_score_plans(HpsInstance* in, const uint8_t* d_plans, int64_t n, const HpsPlanResults* r,
+                    void* stream) {
+  if (!in || !r || !r->cost || !r->status || n < 0) return set_err(HPS_E_INVALID_ARG, "null argument");
+  if (n == 0) return HPS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  PlanSource src{};
+  src.mode = 0;
+  src.plans = d_plans;
+  Outputs o{r->cost, r->status, r->gap, r->ps, r->num_stages, r->k};
+  const unsigned cap = (unsigned)std::min<int64_t>(n, (int64_t)kSlowCap);
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync(&buf, sizeof(unsigned long long) * cap + 64, st));
+  unsigned long long* list = reinterpret_cast<unsigned long long*>(buf);
+  unsigned int* count = reinterpret_cast<unsigned int*>(list + cap);
+  CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
+  Pending pend{list, count, cap};
+  int rc = dispatch_eval<false>(in, src, (uint64_t)n, o, pend, 0, nullptr, grid_for(in, n), st);
+  if (rc) return rc;
+  rc = run_slow(in, src, o, pend, 0, 0, nullptr, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaFreeAsync(buf, st));
+  return HPS_OK;
+}
+
+int hps_enum_argmin(HpsInstance* in, uint64_t begin, uint64_t end, int32_t feasible_only,
+                    HpsArgmin* d_best, void* stream) {
+  if (!in || !d_best || end < begin) return set_err(HPS_E_INVALID_ARG, "bad range");
+  // T^L must fit in 64 bits
+  long double total = powl((long double)in->c.T, (long double)in->c.L);
+  if (total > 1.8e19L) return set_err(HPS_E_CONFIG, "T^L does not fit a 64-bit enumeration index");
+  uint64_t tot = 1;
+  for (int l = 0; l < in->c.L; l++) tot *= (uint64_t)in->c.T;
+  if (end > tot) return set_err(HPS_E_INVALID_ARG, "range beyond T^L");
+  PlanSource src{};
+  src.mode = 1;
+  src.begin = begin;
+  uint64_t pw = 1;
+  for (int l = in->c.L - 1; l >= 0; l--) { src.tpow[l] = pw; pw *= (uint64_t)in->c.T; }
+  return argmin_common(in, src, end - begin, feasible_only, d_best, (cudaStream_t)stream);
+}
+
+int hps_plans_argmin(HpsInstance* in, const uint8_t* d_plans, int64_t n, int32_t feasible_only,
+                     HpsArgmin* d_best, void* stream) {
+  if (!in || !d_best || n < 0) return set_err(HPS_E_INVALID_ARG, "null argument");
+  PlanSource src{};
+  src.mode = 0;
+  src.plans = d_plans;
+  int b = 0;
+  while ((1 << b) < in->c.T) b++;
+  src.tbits = b > 0 ? b : 1;
+  if (src.tbits * in->c.L > 128) return set_err(HPS_E_CONFIG, "assignment rank exceeds 128 bits");
+  return argmin_common(in, src, (uint64_t)n, feasible_only, d_best, (cudaStream_t)stream);
+}
+
+int hps_random_argmin(HpsInstance* in, const HpsPcg64* g, uint64_t first, uint64_t n,
+                      HpsArgmin* d_best, void* stream) {
+  if (!in || !g || !d_best) return set_err(HPS_E_INVALID_ARG, "null argument");
+  if (in->c.T & (in->c.T - 1)) return set_err(HPS_E_CONFIG, "in-kernel plan generation needs a power-of-two T");
+  PlanSource src{};
+  fill_random_source(in, g, first, src);
+  if (src.tbits * in->c.L > 128) return set_err(HPS_E_CONFIG, "assignment rank exceeds 128 bits");
+  return argmin_common(in, src, n, 0, d_best, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void gen_plans_kernel(const InstanceConsts c, const PlanSource src, uint64_t n, uint8_t* out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t p = gw; p < n; p += nw) {
+    int d0, d1;
+    u128 rank;
+    load_digits(c, src, p, d0, d1, rank);
+    if (lane < c.L) out[p * c.L + lane] = (uint8_t)d0;
+    if (lane + 32 < c.L) out[p * c.L + lane + 32] = (uint8_t)d1;
+  }
+}
+
+__global__ void report_kernel(const InstanceConsts c, const DeviceTables tb, const uint8_t* plans,
+                              const int32_t* k, const int32_t* ps, int64_t n, double* ct, double* dt,
+                              double* et, double* tp, double* ptp, double* exec, double* cost,
+                              uint8_t* feasible) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int L = c.L;
+  const uint8_t* pl = plans + i * L;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  int s = 0, start = 0;
+  double overall = inf;
+  int order[kMaxT];
+  long long tot[kMaxT];
+  int nt = 0;
+  unsigned seen = 0;
+  for (int pos = 1; pos <= L; pos++) {
+    if (pos < L && pl[pos] == pl[start]) continue;
+    const int t = pl[start];
+    const StageEntry& e = tb.stages[entry_index(c.P, t, start, pos - 1)];
+    const double kk = (double)k[i * L + s];
+    const double a = e.c_oct * (e.oma + e.alpha / kk), b = e.c_odt * (e.omb + e.beta / kk);
+    const double x = pmax(a, b);
+    const double tpp = (x > 0) ? c.batch / x : inf;
+    ct[i * L + s] = a; dt[i * L + s] = b; et[i * L + s] = x; tp[i * L + s] = tpp;
+    overall = (s == 0) ? tpp : pmin(overall, tpp);
+    if (!(seen >> t & 1u)) { seen |= 1u << t; order[nt] = t; tot[nt] = 0; nt++; }
+    for (int j = 0; j < nt; j++) if (order[j] == t) { tot[j] += k[i * L + s]; break; }
+    s++;
+    start = pos;
+  }
+  const int pcount = ps ? ps[i] : 0;
+  if (pcount > 0 && c.ps_type >= 0) {
+    const int t = c.ps_type;
+    if (!(seen >> t & 1u)) { seen |= 1u << t; order[nt] = t; tot[nt] = 0; nt++; }
+    for (int j = 0; j < nt; j++) if (order[j] == t) { tot[j] += pcount; break; }
+  }
+  const double ex = (overall > 0 && overall != inf) ? c.work / overall : 0.0;
+  double per_second = 0.0;
+  bool quota_ok = true;
+  for (int j = 0; j < nt; j++) {
+    per_second += c.price_h[order[j]] / 3600.0 * (double)tot[j];
+    if (tot[j] > c.quota[order[j]]) quota_ok = false;
+  }
+  ptp[i] = overall;
+  exec[i] = ex;
+  cost[i] = ex * per_second;
+  feasible[i] = (overall > c.limit) && quota_ok;
+}
+}  // namespace
+
+extern "C" int hps_random_plans(HpsInstance* in, const HpsPcg64* g, uint64_t first, uint64_t n,
+                                uint8_t* d_plans, void* stream) {
+  if (!in || !g || !d_plans) return set_err(HPS_E_INVALID_ARG, "null argument");
+  if (in->c.T & (in->c.T - 1)) return set_err(HPS_E_CONFIG, "in-kernel plan generation needs a power-of-two T");
+  PlanSource src{};
+  fill_random_source(in, g, first, src);
+  if (n == 0) return HPS_OK;
+  const uint64_t warps = std::min<uint64_t>(n, (uint64_t)in->sm_count * 64);
+  gen_plans_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(in->c, src, n, d_plans);
+  CUDA_TRY(cudaGetLastError());
+  return HPS_OK;
+}
+
+extern "C" int hps_report(HpsInstance* in, const uint8_t* d_plans, const int32_t* d_k, const int32_t* d_ps,
+                          int64_t n, double* d_ct, double* d_dt, double* d_et, double* d_tp,
+                          double* d_pipeline_tp, double* d_exec_time, double* d_cost, uint8_t* d_feasible,
+                          void* stream) {
+  if (!in || n < 0) return set_err(HPS_E_INVALID_ARG, "bad argument");
+  if (n == 0) return HPS_OK;
+  report_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      in->c, in->tb, d_plans, d_k, d_ps, n, d_ct, d_dt, d_et, d_tp, d_pipeline_tp, d_exec_time, d_cost, d_feasible);
+  CUDA_TRY(cudaGetLastError());
+  return HPS_OK;
+}

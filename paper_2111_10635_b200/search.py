@@ -1,0 +1,169 @@
+"""Plan searchers on the device: brute_force and random_search (ls/baselines.py:63-87,230-282).
+
+Both keep the reference's signature, cap, tie rules and returned ScoredPlan. The sweep is one
+fused kernel per GPU (in-kernel plan decode / generation + per-plan scoring + (cost, rank)
+argmin); with ``torch.distributed`` initialised the index range (or the random-plan stream) is
+split into contiguous per-rank shards and the per-rank winners meet in ONE all_gather of
+48-byte keys — the only exchange the path has.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _abi
+from .errors import ConfigError, InfeasibleError, InvariantError, PlanValidationError
+from .instance import argmin_from_bytes, pcg_from_generator
+from .model import ProvisionerConfig, ScoredPlan, SchedulingPlan
+from .scoring import PlanScorer, device_instance
+
+DEFAULT_ENUMERATION_CAP = 2 ** 24  # ls/baselines.py:27
+
+
+def decode_index(index: int, num_types: int, num_layers: int) -> tuple:
+    """itertools.product order: layer 0 is the most significant base-T digit."""
+    digits = []
+    for _ in range(num_layers):
+        index, d = divmod(index, num_types)
+        digits.append(d)
+    return tuple(reversed(digits))
+
+
+def decode_packed(rank: int, num_types: int, num_layers: int) -> tuple:
+    """Inverse of the packed lexicographic rank (ceil(log2 T) bits per layer)."""
+    bits = max(1, (num_types - 1).bit_length())
+    mask = (1 << bits) - 1
+    return tuple((rank >> ((num_layers - 1 - l) * bits)) & mask for l in range(num_layers))
+
+
+def shard_range(begin: int, end: int, rank: int, world: int) -> tuple:
+    """Contiguous shard r of [begin, end) (SURVEY.md §8(e) partitioning)."""
+    n = end - begin
+    return begin + n * rank // world, begin + n * (rank + 1) // world
+
+
+def _dist():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist
+    except ImportError:  # pragma: no cover
+        pass
+    return None
+
+
+def merge_keys(keys: list) -> dict:
+    """Deterministic min over per-rank argmin keys: (cost, rank); sums the counters."""
+    best = None
+    for k in keys:
+        if best is None or (k["cost"], k["rank"]) < (best["cost"], best["rank"]):
+            best = dict(k)
+    best["evaluated"] = sum(k["evaluated"] for k in keys)
+    best["feasible"] = sum(k["feasible"] for k in keys)
+    best["flags"] = 0
+    for k in keys:
+        best["flags"] |= k["flags"]
+    return best
+
+
+def allgather_argmin(buf, group=None) -> dict:
+    """One all_gather of the 48-byte device keys, then the deterministic host merge."""
+    dist = _dist()
+    if dist is None or dist.get_world_size(group) == 1:
+        return argmin_from_bytes(bytes(buf.cpu().numpy().tobytes()))
+    import torch
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(world * buf.numel(), dtype=torch.uint8, device=buf.device)
+        dist.all_gather_into_tensor(out, buf, group=group)
+        raw = out.cpu().numpy().tobytes()
+    else:
+        cpu = buf.cpu()
+        outs = [torch.empty_like(cpu) for _ in range(world)]
+        dist.all_gather(outs, cpu, group=group)
+        raw = b"".join(o.numpy().tobytes() for o in outs)
+    n = buf.numel()
+    return merge_keys([argmin_from_bytes(raw[i * n:(i + 1) * n]) for i in range(world)])
+
+
+def _raise_flags(key: dict):
+    if key["flags"] & 2:
+        raise PlanValidationError("a plan uses a type id or layer profile the instance lacks")
+    if key["flags"] & 1:
+        raise InvariantError("catalog has no CPU-capable resource type")
+
+
+def enumerate_argmin(graph, catalog, params, begin: int, end: int, feasible_only: bool = True,
+                     config: ProvisionerConfig = ProvisionerConfig(), group=None) -> dict:
+    """Sharded enumeration argmin over [begin, end); every rank gets the merged key."""
+    dist = _dist()
+    rank, world = (dist.get_rank(group), dist.get_world_size(group)) if dist else (0, 1)
+    lo, hi = shard_range(begin, end, rank, world)
+    inst = device_instance(graph, catalog, params, config)
+    buf = inst.enum_argmin_async(lo, hi, feasible_only)
+    return allgather_argmin(buf, group)
+
+
+def brute_force(graph, catalog, params, config: ProvisionerConfig = ProvisionerConfig(),
+                enumeration_cap: int = DEFAULT_ENUMERATION_CAP, group=None) -> ScoredPlan:
+    """Cheapest feasible plan over all T^L assignments (ls/baselines.py:63-87)."""
+    T, L = catalog.num_types, graph.num_layers
+    total = T ** L
+    if total > enumeration_cap:
+        raise ConfigError(f"brute force would enumerate {total} plans ({T}^{L}), "
+                          f"cap is {enumeration_cap}")
+    key = enumerate_argmin(graph, catalog, params, 0, total, True, config, group)
+    _raise_flags(key)
+    if not key["cost"] < float("inf"):
+        raise InfeasibleError(f"no feasible plan among {total} enumerated")
+    best = PlanScorer(graph, catalog, params, config)(SchedulingPlan(decode_index(key["rank"], T, L)))
+    if best.cost != key["cost"]:  # the winner is re-scored through the same kernel
+        raise InvariantError("winner re-score disagrees with the sweep")
+    return ScoredPlan(best.plan, best.provisioning, best.cost, best.report, total)
+
+
+def random_search(graph, catalog, params, budget: int, seed: int = 0, dedup: bool = False,
+                  config: ProvisionerConfig = ProvisionerConfig(), group=None) -> ScoredPlan:
+    """Best of ``budget`` random plans, penalties included (ls/baselines.py:230-282)."""
+    if budget < 1:
+        raise ConfigError("random search budget must be >= 1")
+    T, L = catalog.num_types, graph.num_layers
+    rng = np.random.default_rng(seed)
+    inst = device_instance(graph, catalog, params, config)
+    dist = _dist()
+    rank, world = (dist.get_rank(group), dist.get_world_size(group)) if dist else (0, 1)
+    if not dedup and T & (T - 1) == 0 and (max(1, (T - 1).bit_length()) * L) <= 128:
+        # plans generated in-kernel from the generator's PCG64 stream
+        lo, hi = shard_range(0, budget, rank, world)
+        key = allgather_argmin(inst.random_argmin_async(pcg_from_generator(rng), lo, hi - lo), group)
+        count = budget
+    else:
+        # the assignment list is the reference's own RNG stream (ls/baselines.py:252-272)
+        assignments = _reference_assignments(rng, T, L, budget, dedup)
+        import torch
+        arr = torch.from_numpy(np.array(assignments, dtype=np.uint8).reshape(len(assignments), L))
+        lo, hi = shard_range(0, len(assignments), rank, world)
+        key = allgather_argmin(inst.plans_argmin_async(arr[lo:hi], feasible_only=False), group)
+        count = len(assignments)
+    _raise_flags(key)
+    winner = decode_packed(key["rank"], T, L) if T > 1 else (0,) * L
+    best = PlanScorer(graph, catalog, params, config)(SchedulingPlan(winner))
+    return ScoredPlan(best.plan, best.provisioning, best.cost, best.report, count)
+
+
+def _reference_assignments(rng, T, L, budget, dedup):
+    total = T ** L
+    if dedup and total <= 2 ** 20:
+        chosen = rng.permutation(total)[:min(budget, total)]
+        return [decode_index(int(c), T, L) for c in chosen]
+    if dedup:
+        seen, attempts = set(), 0
+        while len(seen) < budget and attempts < 20 * budget:
+            seen.add(tuple(int(g) for g in rng.integers(0, T, L)))
+            attempts += 1
+        return sorted(seen)
+    return [tuple(int(g) for g in rng.integers(0, T, L)) for _ in range(budget)]
+
+
+__all__ = ["brute_force", "random_search", "enumerate_argmin", "allgather_argmin", "merge_keys",
+           "shard_range", "decode_index", "decode_packed", "DEFAULT_ENUMERATION_CAP"]
