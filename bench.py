@@ -95,7 +95,7 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample or 12_000 * threads
+    sample = args.cpu_sample or 80_000 * threads
     for _ in range(max(0, args.warmup)):
         cpu_oracle_rate(max(1000, sample // 10), threads)
     rates, times = [], []
@@ -293,7 +293,7 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
-            sample = args.cpu_sample or 12_000 * threads
+            sample = args.cpu_sample or 80_000 * threads
             rate, dt = cpu_oracle_rate(sample, threads)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                     "sample": f"{sample} consecutive cfg3 enumeration indices "
