@@ -30,6 +30,19 @@ struct __align__(16) StageEntry {
   double serial;  // max((oct/B_o)(1-alpha), (odt/B_o)(1-beta))  (ls/provisioner.py:184-193)
   int32_t valid;  // 0 when a member lacks a profile for the type (PlanValidationError)
   int32_t type;
+  // single-precision constants for the count ESTIMATE that seeds the exact table search
+  float f_rbo, f_rbd;    // B_o / oct, B_o / odt (0 when the work is 0)
+  float f_oma, f_omb, f_alpha, f_beta;
+  int32_t pad0, pad1;
+};
+
+// Per (stage entry, count m) pair of the TE table: et(m) = _stage_et at integer count m, and
+// th(m-1) = theta(m-1) = the smallest double tau with count(tau) <= m-1 (+inf for m == 1).
+// count(tau) = min{m : theta(m) <= tau}; theta is exact: found by bisection over the bit
+// patterns of tau with the exact _floor_count/_iceil (ls/provisioner.py:75-77,150-176).
+struct __align__(16) TEPair {
+  double et;
+  double th;  // theta(m - 1)
 };
 
 // Stage-0 exits of optimize_k1 for an entry starting at layer 0 (ls/provisioner.py:394-397)
@@ -54,14 +67,15 @@ struct InstanceConsts {
   double price_h[kMaxT];  // price_per_hour
   int64_t quota[kMaxT];
   uint8_t is_cpu[kMaxT];
-  int32_t et_cap[kMaxT];  // ET table holds m in [1, et_cap[t]] for stages of type t
-  int64_t et_off[kMaxT];  // ET table offset of type t's block (rows of et_cap[t])
+  int32_t et_cap[kMaxT];  // TE table holds m in [1, et_cap[t] + 1] for stages of type t
+  int64_t te_off[kMaxT];  // TE table offset of type t's block (rows of et_cap[t] + 1)
+  int32_t redux_ok;       // all quotas < 2^24: per-type sums fit 32-bit warp reductions
 };
 
 struct DeviceTables {
   const StageEntry* stages;   // [T * P]
   const Stage0Info* stage0;   // [T * L] indexed by (t, last)
-  const double* et;           // ET[e][m-1] = max(ct, dt) at integer count m
+  const TEPair* te;           // TE[e][m-1], m = 1 .. et_cap[t] + 1 (same offsets, stride cap+1)
   const int32_t* cls;         // [T * P] ET-equivalence class: entries with bitwise-equal
                               // (oct, odt, alpha, beta) share counts and breakpoints
 };
@@ -125,14 +139,19 @@ __device__ __forceinline__ double count_at(const StageEntry& s, double tau, doub
   return floor_count(s, tau, bo, r, g) ? iceil(r) : __longlong_as_double(0x7ff0000000000000LL);
 }
 
+__device__ __forceinline__ const TEPair* te_row(const InstanceConsts& c, const DeviceTables& tb,
+                                                int t, int e);
+
 __device__ __forceinline__ double et_lookup(const InstanceConsts& c, const DeviceTables& tb,
                                             const StageEntry& s, int e, double k) {
   const int t = s.type;
-  if (k <= (double)c.et_cap[t]) {
-    const int64_t pe = e - t * c.P;  // entry within type block
-    return __ldg(tb.et + c.et_off[t] + pe * (int64_t)c.et_cap[t] + ((int64_t)k - 1));
-  }
+  if (k <= (double)c.et_cap[t] + 1.0) return te_row(c, tb, t, e)[(int64_t)k - 1].et;
   return stage_et(s, k);
+}
+
+__device__ __forceinline__ const TEPair* te_row(const InstanceConsts& c, const DeviceTables& tb,
+                                                int t, int e) {
+  return tb.te + c.te_off[t] + (int64_t)(e - t * c.P) * (int64_t)(c.et_cap[t] + 1);
 }
 
 __device__ __forceinline__ uint64_t sat_count(double k) {  // saturating u64 of a count

@@ -95,6 +95,157 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
+constexpr int kOver = 0x7fffffff;  // "count above quota (or _floor_count raised)"
+
+// single-precision seed of count(tau); correctness never depends on it
+__device__ __forceinline__ int est_count(const StageEntry& s, double tau) {
+  const float t = (float)tau;
+  float q = 1.0f;
+  if (s.oct != 0) {
+    const float h = t * s.f_rbo - s.f_oma;
+    q = (h > 0.f) ? fmaxf(q, __fdividef(s.f_alpha, h)) : 3.0e38f;
+  }
+  if (s.odt != 0) {
+    const float h = t * s.f_rbd - s.f_omb;
+    q = (h > 0.f) ? fmaxf(q, __fdividef(s.f_beta, h)) : 3.0e38f;
+  }
+  const float cf = ceilf(q - 1e-9f);
+  return (cf < 2.0e9f && cf == cf) ? (int)cf : 2000000000;
+}
+
+// Exact count(tau) given count(tau) in [lo, hi] (hi <= table cap). row[c].th = theta(c).
+__device__ __forceinline__ int count_tab(const TEPair* row, double tau, int lo, int hi, int g) {
+  if (lo >= hi) return lo;
+  const int m = min(max(g, lo), hi);
+  if (row[m].th <= tau) {  // count <= m: gallop down
+    int hb = m, lb, step = 1;
+    for (;;) {
+      const int cnd = hb - step;
+      if (cnd < lo) { lb = lo - 1; break; }
+      if (row[cnd].th <= tau) { hb = cnd; step <<= 1; } else { lb = cnd; break; }
+    }
+    while (hb - lb > 1) { const int md = (lb + hb) >> 1; if (row[md].th <= tau) hb = md; else lb = md; }
+    return hb;
+  }
+  int lb = m, hb, step = 1;  // count > m: gallop up (count <= hi is guaranteed)
+  for (;;) {
+    const int cnd = lb + step;
+    if (cnd >= hi) { hb = hi; break; }
+    if (row[cnd].th <= tau) { hb = cnd; break; }
+    lb = cnd;
+    step <<= 1;
+  }
+  while (hb - lb > 1) { const int md = (lb + hb) >> 1; if (row[md].th <= tau) hb = md; else lb = md; }
+  return hb;
+}
+
+// per-type sums of counts <= quota for all types (lanes own stages r and r+32)
+__device__ __forceinline__ bool quota_sums_ok(const InstanceConsts& c, unsigned types_present,
+                                              int t0, int k0, int t1, int k1) {
+  bool ok = true;
+  while (types_present) {
+    const int t = __ffs(types_present) - 1;
+    types_present &= types_present - 1;
+    const unsigned v = (t0 == t ? (unsigned)k0 : 0u) + (t1 == t ? (unsigned)k1 : 0u);
+    const unsigned sum = __reduce_add_sync(0xffffffffu, v);
+    ok = ok && ((long long)sum <= c.quota[t]);
+  }
+  return ok;
+}
+
+// Bisection on quota_ok (ls/provisioner.py:430-437). Inputs: counts at tau_hi in kb[] (finite,
+// quota-feasible). Output: tau_lo and the counts at tau_lo.
+__device__ double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, const StageEntry* st,
+                              const int32_t* ent, int S, double a, double b, const double kb_in[2],
+                              int kb_out[2]) {
+  const int lane = threadIdx.x & 31;
+  int lb[2], ub[2], ty[2] = {-1, -1}, Q[2] = {0, 0};
+  const TEPair* row[2] = {nullptr, nullptr};
+  double thq[2] = {0.0, 0.0};
+  unsigned present = 0;
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    lb[slot] = ub[slot] = 0;
+    if (s < S) {
+      ty[slot] = st[s].type;
+      Q[slot] = (int)c.quota[ty[slot]];
+      row[slot] = te_row(c, tb, ty[slot], ent[s]);
+      lb[slot] = (int)kb_in[slot];
+      ub[slot] = kOver;
+      thq[slot] = row[slot][Q[slot]].th;  // count <= Q  <=>  tau >= theta(Q)
+    }
+  }
+  present = __reduce_or_sync(0xffffffffu, (ty[0] >= 0 ? 1u << ty[0] : 0u) | (ty[1] >= 0 ? 1u << ty[1] : 0u));
+  int it = 0;
+  for (; it < 60; it++) {
+    const bool wide = (ub[0] - lb[0] > 1 && ub[0] != kOver) || (ub[1] - lb[1] > 1 && ub[1] != kOver) ||
+                      (ub[0] == kOver && lb[0] < Q[0]) || (ub[1] == kOver && lb[1] < Q[1]);
+    if (!__any_sync(0xffffffffu, wide)) break;
+    const double mid = (a + b) / 2.0;
+    int km[2];
+    bool over = false;
+    for (int slot = 0; slot < 2; slot++) {
+      km[slot] = lb[slot];
+      if (ub[slot] != lb[slot]) {
+        if (ub[slot] == kOver && mid < thq[slot]) {
+          km[slot] = kOver;
+          over = true;
+        } else {
+          const int s = lane + 32 * slot;
+          const int hi = (ub[slot] == kOver) ? Q[slot] : ub[slot];
+          km[slot] = count_tab(row[slot], mid, lb[slot], hi, est_count(st[s], mid));
+        }
+      }
+    }
+    const bool any_over = __any_sync(0xffffffffu, over);
+    const bool ok = !any_over && quota_sums_ok(c, present, ty[0], km[0], ty[1], km[1]);
+    if (ok) { b = mid; lb[0] = km[0]; lb[1] = km[1]; }
+    else { a = mid; ub[0] = km[0]; ub[1] = km[1]; }
+  }
+  if (it < 60) {
+    // every unpinned stage has count(a) == count(b) + 1 (or "over" with count(b) == Q):
+    // on (a, b) its count is lb + [tau < theta(lb)], so quota_ok switches at one of those
+    // thresholds (or stays true up to b). Find the switch point tau* exactly.
+    double cand[2] = {__longlong_as_double(0x7ff0000000000000LL), __longlong_as_double(0x7ff0000000000000LL)};
+    double thr_lb[2] = {0.0, 0.0};
+    for (int slot = 0; slot < 2; slot++) {
+      if (ub[slot] != lb[slot]) {
+        thr_lb[slot] = row[slot][lb[slot]].th;  // count <= lb  <=>  tau >= theta(lb)
+        if (thr_lb[slot] > a && thr_lb[slot] <= b) cand[slot] = thr_lb[slot];
+      }
+    }
+    double tstar = b;
+    // candidates in ascending order; the predicate is monotone, so the first true one wins
+    double lo_bound = -__longlong_as_double(0x7ff0000000000000LL);
+    for (;;) {
+      // next smallest candidate above lo_bound
+      double mine = fmin(cand[0] > lo_bound ? cand[0] : __longlong_as_double(0x7ff0000000000000LL),
+                         cand[1] > lo_bound ? cand[1] : __longlong_as_double(0x7ff0000000000000LL));
+      const double x = warp_min(mine);
+      if (!(x < b)) break;  // b itself is feasible
+      int kx[2];
+      bool ov = false;
+      for (int slot = 0; slot < 2; slot++) {
+        kx[slot] = lb[slot];
+        if (ub[slot] != lb[slot] && x < thr_lb[slot]) { kx[slot] = ub[slot]; ov |= (ub[slot] == kOver); }
+      }
+      const bool okx = !__any_sync(0xffffffffu, ov) && quota_sums_ok(c, present, ty[0], kx[0], ty[1], kx[1]);
+      if (okx) { tstar = x; break; }
+      lo_bound = x;
+    }
+    for (; it < 60; it++) {
+      const double mid = (a + b) / 2.0;
+      if (mid >= tstar) b = mid; else a = mid;
+    }
+    for (int slot = 0; slot < 2; slot++)
+      if (ub[slot] != lb[slot] && b < thr_lb[slot]) lb[slot] = ub[slot];
+  }
+  kb_out[0] = lb[0];
+  kb_out[1] = lb[1];
+  return b;
+}
+
+
 // Evaluate one candidate tau: numpy _best_candidate column (ls/provisioner.py:286-308).
 // Returns +inf when the column is not ok (throughput <= limit).
 template <int MAXS>
@@ -118,7 +269,7 @@ __device__ __forceinline__ double candidate_cost(const InstanceConsts& c, const 
 // Phase A: stages, optimize_k1 exits and the bisection. Returns false when the plan is
 // finished (infeasible / invalid); otherwise fills w.kmin/kmax and tau_lo/tau_hi.
 // Lane l holds digits d0 (layer l) and d1 (layer l+32).
-template <int MAXS>
+template <int MAXS, bool FAST = false>
 __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables& tb,
                                     WarpSmem<MAXS>& w, int d0, int d1, PlanOut& out,
                                     double& tau_lo_out, double& tau_hi_out, int& n_cand) {
@@ -236,24 +387,31 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
   }
   // --- bisection (ls/provisioner.py:430-437); counts monotone in tau => pinning ---
   double a = ser, b = tau_hi;
-  for (int it = 0; it < 60; it++) {
-    const double mid = (a + b) / 2.0;
-    double km[2] = {inf, inf};
-    bool rz = false;
-    if (lane < kMaxT) w.tsum[lane] = 0ull;
-    __syncwarp();
-    for (int slot = 0; slot < 2; slot++) {
-      const int s = lane + 32 * slot;
-      if (s < S) {
-        km[slot] = (ka[slot] == kb[slot]) ? kb[slot] : count_at(w.st[s], mid, c.bo);
-        if (km[slot] == inf) rz = true; else atomicAdd(&w.tsum[w.st[s].type], sat_count(km[slot]));
+  if (FAST) {
+    int kl[2];
+    b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
+    kb[0] = (double)kl[0];
+    kb[1] = (double)kl[1];
+  } else {
+    for (int it = 0; it < 60; it++) {
+      const double mid = (a + b) / 2.0;
+      double km[2] = {inf, inf};
+      bool rz = false;
+      if (lane < kMaxT) w.tsum[lane] = 0ull;
+      __syncwarp();
+      for (int slot = 0; slot < 2; slot++) {
+        const int s = lane + 32 * slot;
+        if (s < S) {
+          km[slot] = (ka[slot] == kb[slot]) ? kb[slot] : count_at(w.st[s], mid, c.bo);
+          if (km[slot] == inf) rz = true; else atomicAdd(&w.tsum[w.st[s].type], sat_count(km[slot]));
+        }
       }
+      __syncwarp();
+      bool bad = rz || ((lane < c.T) && (w.tsum[lane] > (unsigned long long)c.quota[lane]));
+      const bool ok = !__any_sync(0xffffffffu, bad);
+      if (ok) { b = mid; kb[0] = km[0]; kb[1] = km[1]; }
+      else { a = mid; ka[0] = km[0]; ka[1] = km[1]; }
     }
-    __syncwarp();
-    bool bad = rz || ((lane < c.T) && (w.tsum[lane] > (unsigned long long)c.quota[lane]));
-    const bool ok = !__any_sync(0xffffffffu, bad);
-    if (ok) { b = mid; kb[0] = km[0]; kb[1] = km[1]; }
-    else { a = mid; ka[0] = km[0]; ka[1] = km[1]; }
   }
   const double tau_lo = b;
   // --- m_min / m_max and class leaders (ls/provisioner.py:442-455) ---
@@ -351,7 +509,7 @@ __device__ double phase_candidates(const InstanceConsts& c, const DeviceTables& 
 
 // Phase C: counts at the chosen tau, add_ps_cores (ls/provisioner.py:486-513) and the final
 // evaluate() whose monetary_cost is the score (ls/scoring.py:96-97, ls/costmodel.py:102-167).
-template <int MAXS>
+template <int MAXS, bool FAST = false>
 __device__ void phase_final(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
                             int S, double tau, PlanOut& out) {
   const int lane = threadIdx.x & 31;
@@ -359,7 +517,15 @@ __device__ void phase_final(const InstanceConsts& c, const DeviceTables& tb, War
   long long accel = 0, on_ps = 0;
   double emax = 0.0;
   for (int s = lane; s < S; s += 32) {
-    double k = (w.kmin[s] == w.kmax[s]) ? w.kmin[s] : count_at(w.st[s], tau, c.bo);
+    double k = w.kmin[s];
+    if (w.kmax[s] != k) {
+      if (FAST) {
+        const TEPair* row = te_row(c, tb, w.st[s].type, w.ent[s]);
+        k = (double)count_tab(row, tau, (int)w.kmin[s], (int)w.kmax[s], est_count(w.st[s], tau));
+      } else {
+        k = count_at(w.st[s], tau, c.bo);
+      }
+    }
     w.kres[s] = k;
     const int t = w.st[s].type;
     if (!c.is_cpu[t]) accel += (long long)k;

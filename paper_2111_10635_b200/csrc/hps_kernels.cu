@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -22,7 +23,7 @@
 #include <tuple>
 #include <vector>
 
-#include "hps_eval.cuh"
+#include "hps_sweep.cuh"
 
 using namespace hps;
 
@@ -43,7 +44,6 @@ int set_err(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kEtCapMax = 16384;
-constexpr int kSlowBlocks = 32;
 constexpr int kSlowThreads = 256;
 
 // ------------------------------------------------------------------ plan sources
@@ -185,12 +185,13 @@ __device__ __forceinline__ void write_plan(const InstanceConsts& c, const WarpSm
 
 // ------------------------------------------------------------------ K1 / K2
 
-template <int MAXS, int WARPS, bool ARGMIN>
+template <int MAXS, int WARPS, bool ARGMIN, bool FAST>
 __global__ void __launch_bounds__(WARPS * 32)
 eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, uint64_t n,
             Outputs o, Pending pend, int feasible_only, KeyPart* parts) {
-  __shared__ WarpSmem<MAXS> sm[WARPS];
-  __shared__ KeyPart bparts[WARPS];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
+  SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmem<MAXS>) * WARPS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSmem<MAXS>& w = sm[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
@@ -205,7 +206,8 @@ eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
     u128 rank;
     load_digits(c, src, p, d0, d1, rank);
     PlanOut r;
-    eval_plan_warp<MAXS>(c, tb, w, d0, d1, r);
+    if (FAST) eval_plan_fast<MAXS>(c, tb, w, ss[warp], d0, d1, r);
+    else eval_plan_warp<MAXS>(c, tb, w, d0, d1, r);
     if (r.status == kStPending) {
       if (lane == 0) {
         unsigned int at = atomicAdd(pend.count, 1u);
@@ -226,19 +228,7 @@ eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
     }
     __syncwarp();
   }
-  if (ARGMIN) {
-    if (lane == 0) bparts[warp] = KeyPart{best, 0ull, feas, flags};
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      KeyPart acc = bparts[0];
-      for (int i = 1; i < WARPS; i++) {
-        if (key_less(bparts[i].best, acc.best)) acc.best = bparts[i].best;
-        acc.feasible += bparts[i].feasible;
-        acc.flags |= bparts[i].flags;
-      }
-      parts[blockIdx.x] = acc;
-    }
-  }
+  if (ARGMIN && lane == 0) parts[gw] = KeyPart{best, 0ull, feas, flags};  // one partial per warp
 }
 
 // ------------------------------------------------------------------ K7 slow path
@@ -597,6 +587,13 @@ __global__ void stage_table_kernel(const InstanceConsts c, RawTables raw, StageE
   e.serial = pmax(e.c_oct * e.oma, e.c_odt * e.omb);
   e.valid = valid ? 1 : 0;
   e.type = t;
+  e.f_rbo = (e.oct != 0) ? (float)(c.bo / e.oct) : 0.f;
+  e.f_rbd = (e.odt != 0) ? (float)(c.bo / e.odt) : 0.f;
+  e.f_oma = (float)e.oma;
+  e.f_omb = (float)e.omb;
+  e.f_alpha = (float)e.alpha;
+  e.f_beta = (float)e.beta;
+  e.pad0 = e.pad1 = 0;
   out[idx] = e;
 }
 
@@ -632,14 +629,31 @@ __global__ void stage0_kernel(const InstanceConsts c, const StageEntry* st, Stag
   out[idx] = r;
 }
 
-__global__ void et_table_kernel(const InstanceConsts c, const StageEntry* st, double* et, int t,
-                                int64_t count) {
+// TE[e][m-1] = {et(m), theta(m-1)}; theta(j) = min{tau >= 0 : count(tau) <= j}, found by
+// bisection over the bit patterns of non-negative doubles with the exact count function
+// (count is monotone in tau, so the predicate is monotone in the bit pattern).
+__device__ double theta_exact(const StageEntry& s, double bo, double j) {
+  if (count_at(s, 0.0, bo) <= j) return 0.0;
+  unsigned long long lo = 0ull, hi = 0x7ff0000000000000ull;  // pred(lo) false, pred(hi) true
+  while (hi - lo > 1ull) {
+    const unsigned long long mid = lo + ((hi - lo) >> 1);
+    if (count_at(s, __longlong_as_double((long long)mid), bo) <= j) hi = mid; else lo = mid;
+  }
+  return __longlong_as_double((long long)hi);
+}
+
+__global__ void te_table_kernel(const InstanceConsts c, const StageEntry* st, TEPair* te, int t,
+                                int64_t count, int64_t off) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= count) return;
-  const int cap = c.et_cap[t];
-  const int64_t pe = idx / cap;
-  const double m = (double)(idx % cap + 1);
-  et[c.et_off[t] + idx] = stage_et(st[t * c.P + pe], m);
+  const int rows = c.et_cap[t] + 1;
+  const int64_t pe = idx / rows;
+  const int m = (int)(idx % rows) + 1;
+  const StageEntry& s = st[t * c.P + pe];
+  TEPair p;
+  p.et = stage_et(s, (double)m);
+  p.th = (m == 1) ? __longlong_as_double(0x7ff0000000000000LL) : theta_exact(s, c.bo, (double)(m - 1));
+  te[off + idx] = p;
 }
 
 }  // namespace
@@ -651,19 +665,22 @@ struct HpsInstance {
   DeviceTables tb;
   StageEntry* d_stages = nullptr;
   Stage0Info* d_stage0 = nullptr;
-  double* d_et = nullptr;
+  TEPair* d_te = nullptr;
   int32_t* d_cls = nullptr;
+  bool fast = false;
   std::vector<StageEntry> h_stages;
   int sm_count = 148;
 };
 
 namespace {
 
-template <int MAXS, int WARPS, bool ARGMIN>
+template <int MAXS, int WARPS, bool ARGMIN, bool FAST>
 int launch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
                 int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
-  eval_kernel<MAXS, WARPS, ARGMIN><<<grid, WARPS * 32, 0, st>>>(in->c, in->tb, src, n, o, pend,
-                                                                feasible_only, parts);
+  const size_t smem = sizeof(WarpSmem<MAXS>) * WARPS + (FAST ? sizeof(SweepSmem<MAXS>) * WARPS : 0);
+  auto kern = eval_kernel<MAXS, WARPS, ARGMIN, FAST>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, WARPS * 32, smem, st>>>(in->c, in->tb, src, n, o, pend, feasible_only, parts);
   CUDA_TRY(cudaGetLastError());
   return HPS_OK;
 }
@@ -671,15 +688,22 @@ int launch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Output
 template <bool ARGMIN>
 int dispatch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
                   int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
-  if (in->c.L <= 16) return launch_eval<16, 8, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
-  if (in->c.L <= 32) return launch_eval<32, 8, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
-  return launch_eval<64, 4, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (in->fast) {
+    if (in->c.L <= 16) return launch_eval<16, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+    if (in->c.L <= 32) return launch_eval<32, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+    return launch_eval<64, 2, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  }
+  if (in->c.L <= 16) return launch_eval<16, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (in->c.L <= 32) return launch_eval<32, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  return launch_eval<64, 2, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
 }
 
+int warps_per_block(const HpsInstance* in) { return (in->c.L <= 32) ? 4 : 2; }
+
 int grid_for(HpsInstance* in, uint64_t n_plans) {
-  const int warps = (in->c.L <= 32) ? 8 : 4;
+  const int warps = warps_per_block(in);
   uint64_t blocks = (n_plans + warps - 1) / warps;
-  uint64_t cap = (uint64_t)in->sm_count * 8;
+  uint64_t cap = (uint64_t)in->sm_count * 16;
   return (int)std::max<uint64_t>(1, std::min(blocks, cap));
 }
 
@@ -694,8 +718,10 @@ int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending p
              int feasible_only, KeyPart* slow_parts, cudaStream_t st) {
   const size_t per_block = slow_per_block(in);
   double* scratch = nullptr;
-  CUDA_TRY(cudaMallocAsync(&scratch, per_block * kSlowBlocks * sizeof(double), st));
-  slow_kernel<<<kSlowBlocks, kSlowThreads, 0, st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
+  const size_t cap_blocks = std::max<size_t>(8, ((size_t)512 << 20) / (per_block * sizeof(double)));
+  const int blocks = (int)std::min<size_t>((size_t)in->sm_count * 2, cap_blocks);
+  CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
+  slow_kernel<<<blocks, kSlowThreads, 0, st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
                                                     slow_parts, scratch, per_block);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(scratch, st));
@@ -732,12 +758,13 @@ struct ArgminScratch {
 int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_only, HpsArgmin* d_best,
                   cudaStream_t st) {
   const int grid = grid_for(in, n);
+  const int nparts = grid * warps_per_block(in);
   const unsigned cap = (unsigned)std::min<uint64_t>(kSlowCap, std::max<uint64_t>(n, 1));
   char* buf = nullptr;
-  const size_t bytes = sizeof(KeyPart) * (grid + cap) + sizeof(unsigned long long) * cap + 64;
+  const size_t bytes = sizeof(KeyPart) * (nparts + cap) + sizeof(unsigned long long) * cap + 64;
   CUDA_TRY(cudaMallocAsync(&buf, bytes, st));
   KeyPart* parts = reinterpret_cast<KeyPart*>(buf);
-  KeyPart* slow_parts = parts + grid;
+  KeyPart* slow_parts = parts + nparts;
   unsigned long long* list = reinterpret_cast<unsigned long long*>(slow_parts + cap);
   unsigned int* count = reinterpret_cast<unsigned int*>(list + cap);
   CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
@@ -747,7 +774,7 @@ int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_onl
   if (rc) return rc;
   rc = run_slow(in, src, o, pend, 1, feasible_only, slow_parts, st);
   if (rc) return rc;
-  finish_argmin<<<1, 256, 0, st>>>(parts, grid, slow_parts, count, cap, n, d_best);
+  finish_argmin<<<1, 256, 0, st>>>(parts, nparts, slow_parts, count, cap, n, d_best);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(buf, st));
   return HPS_OK;
@@ -811,11 +838,15 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   }
   c.penalty_scale = 1e6 * mx;
   int64_t off = 0;
+  bool fast = true;
   for (int t = 0; t < T; t++) {
     c.et_cap[t] = (int32_t)std::max<int64_t>(1, std::min<int64_t>(d->quota[t], kEtCapMax));
-    c.et_off[t] = off;
-    off += (int64_t)c.P * c.et_cap[t];
+    if (d->quota[t] > kEtCapMax) fast = false;  // counts could leave the threshold table
+    c.te_off[t] = off;
+    off += (int64_t)c.P * (c.et_cap[t] + 1);
   }
+  c.redux_ok = fast ? 1 : 0;
+  in->fast = fast && (getenv("HPS_FORCE_LITERAL") == nullptr);
   // raw tables -> device
   const size_t tl = (size_t)T * L * sizeof(double);
   double* d_raw = nullptr;
@@ -828,15 +859,15 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   const int ne = T * c.P;
   CUDA_TRY(cudaMalloc(&in->d_stages, sizeof(StageEntry) * ne));
   CUDA_TRY(cudaMalloc(&in->d_stage0, sizeof(Stage0Info) * T * L));
-  CUDA_TRY(cudaMalloc(&in->d_et, sizeof(double) * off));
+  CUDA_TRY(cudaMalloc(&in->d_te, sizeof(TEPair) * off));
   CUDA_TRY(cudaMalloc(&in->d_cls, sizeof(int32_t) * ne));
   stage_table_kernel<<<(ne + 127) / 128, 128>>>(c, raw, in->d_stages);
   CUDA_TRY(cudaGetLastError());
   stage0_kernel<<<(T * L + 127) / 128, 128>>>(c, in->d_stages, in->d_stage0);
   CUDA_TRY(cudaGetLastError());
   for (int t = 0; t < T; t++) {
-    const int64_t cnt = (int64_t)c.P * c.et_cap[t];
-    et_table_kernel<<<(unsigned)((cnt + 255) / 256), 256>>>(c, in->d_stages, in->d_et, t, cnt);
+    const int64_t cnt = (int64_t)c.P * (c.et_cap[t] + 1);
+    te_table_kernel<<<(unsigned)((cnt + 127) / 128), 128>>>(c, in->d_stages, in->d_te, t, cnt, c.te_off[t]);
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaDeviceSynchronize());
@@ -856,7 +887,7 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
     cls[e] = it->second;
   }
   CUDA_TRY(cudaMemcpy(in->d_cls, cls.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
-  in->tb = DeviceTables{in->d_stages, in->d_stage0, in->d_et, in->d_cls};
+  in->tb = DeviceTables{in->d_stages, in->d_stage0, in->d_te, in->d_cls};
   *out = in;
   return HPS_OK;
 }
@@ -865,7 +896,7 @@ int hps_instance_destroy(HpsInstance* in) {
   if (!in) return HPS_OK;
   cudaFree(in->d_stages);
   cudaFree(in->d_stage0);
-  cudaFree(in->d_et);
+  cudaFree(in->d_te);
   cudaFree(in->d_cls);
   delete in;
   return HPS_OK;

@@ -178,3 +178,16 @@ def test_scorer_dropin_reports_match_goldens():
     prov = provision(p0, g, c, job)
     rep = evaluate(p0, prov, g, c, job)
     assert rep.monetary_cost.hex() == records[0]["cost"] and rep.feasible
+
+
+@pytest.mark.parametrize("name,n", [("cfg3", 30000), ("cfg5", 3000), ("quota", 20000), ("tightmn", 20000)])
+def test_fast_path_equals_literal_path(name, n, monkeypatch):
+    """The threshold-table sweep (default) and the literal division path agree bit for bit."""
+    g, c, job = instance(name)
+    plans = np.random.default_rng(77).integers(0, c.num_types, (n, g.num_layers)).astype(np.uint8)
+    fast = _score(_dev(g, c, job), plans)
+    monkeypatch.setenv("HPS_FORCE_LITERAL", "1")
+    lit = _score(_dev(g, c, job), plans)
+    for k in ("status", "ps", "k", "num_stages"):
+        assert np.array_equal(fast[k], lit[k]), k
+    assert _same_bits(fast["cost"], lit["cost"]) and _same_bits(fast["gap"], lit["gap"])
