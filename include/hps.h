@@ -165,6 +165,32 @@ int hps_report(HpsInstance* inst, const uint8_t* d_plans, const int32_t* d_k,
                double* d_tp, double* d_pipeline_tp, double* d_exec_time, double* d_cost,
                uint8_t* d_feasible, void* stream);
 
+/* ---- scheduling policy on the device (K3-K6) -----------------------------------------------
+ * Replaces policy_forward / sample_actions / the train() round body / policy_gradient /
+ * policy_backward (ls/policy/network.py:147-262, ls/policy/training.py:115-274). */
+typedef struct HpsPolicy HpsPolicy;
+int hps_policy_create(int32_t num_layers, int32_t feature_dim, int32_t hidden, int32_t num_types,
+                      int32_t lstm, int64_t max_plans, const double* features, HpsPolicy** out);
+int hps_policy_destroy(HpsPolicy* policy);
+/* which: 0 w_cell [D+H][G*H], 1 b_cell, 2 w_out [H][T], 3 b_out; dir 0 host->device, 1 back */
+int hps_policy_params(HpsPolicy* policy, int32_t which, int32_t dir, double* host, int64_t n);
+/* K4: LSTM/Elman forward at the current parameters; probabilities [L][T] to d_probs (optional) */
+int hps_policy_forward(HpsPolicy* policy, double temperature, double* d_probs, void* stream);
+/* K3: n plans; plan g, layer t uses draw first_draw + g*L + t of the PCG64 stream, one
+ * Generator.random() per Generator.choice(T, p) */
+int hps_policy_sample(HpsPolicy* policy, const HpsPcg64* gen, uint64_t first_draw, int64_t n,
+                      uint8_t* d_plans, void* stream);
+/* K6+K5: one REINFORCE round from the G scored plans: best-ever, winsorising, standardising,
+ * dlogits in trace order, BPTT, norm cap, update, moving-average baseline, RoundStats row */
+int hps_policy_reinforce(HpsPolicy* policy, const double* d_cost, const uint8_t* d_status,
+                         const uint8_t* d_plans, int64_t num_plans, int32_t round,
+                         double temperature, double learning_rate, double baseline_rate,
+                         double* d_history, uint8_t* d_best_plan, long long* d_best_where,
+                         void* stream);
+/* {baseline, best cost, entropy} and {non-finite logits, non-finite params} flags */
+int hps_policy_state(HpsPolicy* policy, double* state3, int32_t* flags2);
+const char* hps_policy_last_error(void);
+
 /* FP64 pipe microbenchmark (kind 0: dependent-chain DFMA x8 per thread, 16 flops per loop
  * step per chain pair; kind 1: IEEE division). Used for the roofline denominator. */
 int hps_probe_fp64(int kind, double* d_out, int blocks, int threads, int iters, void* stream);

@@ -137,6 +137,18 @@ _SIGNATURES = {
                                     C.c_void_p, C.c_void_p]),
     "hps_random_plans": (C.c_int, [C.c_void_p, C.POINTER(HpsPcg64), C.c_uint64, C.c_uint64,
                                    C.c_void_p, C.c_void_p]),
+    "hps_policy_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "hps_policy_destroy": (C.c_int, [C.c_void_p]),
+    "hps_policy_params": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64]),
+    "hps_policy_forward": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
+    "hps_policy_sample": (C.c_int, [C.c_void_p, C.POINTER(HpsPcg64), C.c_uint64, C.c_int64,
+                                    C.c_void_p, C.c_void_p]),
+    "hps_policy_reinforce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                       C.c_int32, C.c_double, C.c_double, C.c_double, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hps_policy_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hps_policy_last_error": (C.c_char_p, []),
     "hps_probe_fp64": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),
 }

@@ -34,7 +34,61 @@ struct __align__(16) StageEntry {
   float f_rbo, f_rbd;    // B_o / oct, B_o / odt (0 when the work is 0)
   float f_oma, f_omb, f_alpha, f_beta;
   int32_t pad0, pad1;
+  double rwo, rwd;       // fl(1/oct), fl(1/odt) (0 when the work is 0): certified counts
 };
+
+// Certified count: q = frac / (fl(fl(tau*bo)/work) - (1-frac)) evaluated with a reciprocal
+// instead of the two IEEE divisions, together with a rigorous bound on its distance to the
+// reference's value; when ceil(fl(v - 1e-9)) cannot change inside the bound the integer count
+// is exact (monotone ops). Returns -1 when uncertain (caller falls back to the exact path).
+// Valid only where the stage does not raise (tau inside [tau_lo, tau_hi] or above a point
+// known not to raise), which is where callers use it.
+__device__ __forceinline__ double rcp_refined(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);  // two Newton steps: error 2^-22 -> 2^-44 -> rounding level
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+static __device__ __noinline__ int count_cert(const StageEntry& s, double tau, double bo) {
+  const double A = tau * bo;  // identical to the reference's first product
+  double lo = 1.0, hi = 1.0;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const double work = side ? s.odt : s.oct;
+    if (work == 0) continue;
+    const double frac = side ? s.beta : s.alpha;
+    const double omf = side ? s.omb : s.oma;
+    const double B = A * (side ? s.rwd : s.rwo);
+    const double h = B - omf;
+    if (frac == 0.0) {
+      // side is skipped when headroom >= 0; decide exactly only if clearly so
+      if (h > 4e-16 * (B + 1.0)) continue;
+      return -1;
+    }
+    const double eh = (4.0 * B + 3.0 * fabs(h)) * 1.1102230246251565e-16;  // |h - h_ref| bound
+    if (!(h > 2.0 * eh)) return -1;
+    const double rh = rcp_refined(h);
+    const double q = frac * rh;
+    // |q - q_ref| <= q (eh/(h-eh) + 4u) and eh/(h-eh) <= 2 eh/h since h > 2 eh
+    const double dq = q * fma(2.02 * eh, rh, 8.0 * 1.1102230246251565e-16);
+    lo = fmax(lo, q - dq);
+    hi = fmax(hi, q + dq);
+  }
+  const double c_lo = ceil(lo - 1e-9), c_hi = ceil(hi - 1e-9);
+  if (c_lo != c_hi || !(c_hi < 2.0e9)) return -1;
+  return c_lo < 1.0 ? 1 : (int)c_lo;
+}
+
+// et(k) approximately (k >= 1 integer): within ~4 ulp of _stage_et(s, k)
+__device__ __forceinline__ double et_approx(const StageEntry& s, double k) {
+  const double rk = rcp_refined(k);
+  const double ct = s.c_oct * fma(s.alpha, rk, s.oma);
+  const double dt = s.c_odt * fma(s.beta, rk, s.omb);
+  return fmax(ct, dt);
+}
 
 // Per (stage entry, count m) pair of the TE table: et(m) = _stage_et at integer count m, and
 // th(m-1) = theta(m-1) = the smallest double tau with count(tau) <= m-1 (+inf for m == 1).
@@ -168,7 +222,7 @@ __device__ __forceinline__ u128 dbl_to_u128(double x) {
 }
 
 // Python int/int true division (correctly rounded), 0 <= n < 2^127, d > 0.
-__device__ inline double int_true_div(u128 n, int64_t d) {
+static __device__ __noinline__ double int_true_div(u128 n, int64_t d) {
   if (n < ((u128)1 << 53)) return (double)(uint64_t)n / (double)d;
   u128 q = n / (u128)d, r = n % (u128)d;
   int e = 0;

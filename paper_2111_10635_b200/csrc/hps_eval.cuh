@@ -49,7 +49,7 @@ struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min
   bool overflow;
   double mn;
   __device__ __forceinline__ void init() { n = 0; overflow = false; mn = __longlong_as_double(0x7ff0000000000000LL); }
-  __device__ __forceinline__ void insert(double cost, double tau) {
+  __device__ __noinline__ void insert(double cost, double tau) {
     if (!(cost <= mn + 1e-15) && n > 0) return;  // cannot be within 1e-15 of the minimum
     if (cost < mn) {
       mn = cost;
@@ -114,7 +114,7 @@ __device__ __forceinline__ int est_count(const StageEntry& s, double tau) {
 }
 
 // Exact count(tau) given count(tau) in [lo, hi] (hi <= table cap). row[c].th = theta(c).
-__device__ __forceinline__ int count_tab(const TEPair* row, double tau, int lo, int hi, int g) {
+static __device__ __noinline__ int count_tab(const TEPair* row, double tau, int lo, int hi, int g) {
   if (lo >= hi) return lo;
   const int m = min(max(g, lo), hi);
   if (row[m].th <= tau) {  // count <= m: gallop down
@@ -155,7 +155,7 @@ __device__ __forceinline__ bool quota_sums_ok(const InstanceConsts& c, unsigned 
 
 // Bisection on quota_ok (ls/provisioner.py:430-437). Inputs: counts at tau_hi in kb[] (finite,
 // quota-feasible). Output: tau_lo and the counts at tau_lo.
-__device__ double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, const StageEntry* st,
+static __device__ __noinline__ double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, const StageEntry* st,
                               const int32_t* ent, int S, double a, double b, const double kb_in[2],
                               int kb_out[2]) {
   const int lane = threadIdx.x & 31;
@@ -193,7 +193,8 @@ __device__ double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, c
         } else {
           const int s = lane + 32 * slot;
           const int hi = (ub[slot] == kOver) ? Q[slot] : ub[slot];
-          km[slot] = count_tab(row[slot], mid, lb[slot], hi, est_count(st[s], mid));
+          const int kc = count_cert(st[s], mid, c.bo);  // mid >= theta(Q): no raise here
+          km[slot] = (kc >= lb[slot] && kc <= hi) ? kc : count_tab(row[slot], mid, lb[slot], hi, est_count(st[s], mid));
         }
       }
     }

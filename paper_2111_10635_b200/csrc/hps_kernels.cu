@@ -62,13 +62,14 @@ struct PlanSource {
 __host__ __device__ __forceinline__ u128 mk(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
 
 // digits of plan number p (relative to src.begin) for this lane: d0 = layer lane, d1 = lane+32
+template <int MODE>
 __device__ __forceinline__ void load_digits(const InstanceConsts& c, const PlanSource& src,
                                             uint64_t p, int& d0, int& d1, u128& rank) {
   const int lane = threadIdx.x & 31;
   const int L = c.L;
   d0 = 0;
   d1 = 0;
-  if (src.mode == 0) {
+  if (MODE == 0) {
     const uint8_t* row = src.plans + p * (uint64_t)L;
     if (lane < L) d0 = row[lane];
     if (lane + 32 < L) d1 = row[lane + 32];
@@ -86,10 +87,16 @@ __device__ __forceinline__ void load_digits(const InstanceConsts& c, const PlanS
       }
       rank = mk(hi, lo);
     }
-  } else if (src.mode == 1) {
+  } else if (MODE == 1) {
     const uint64_t idx = src.begin + p;
-    if (lane < L) d0 = (int)((idx / src.tpow[lane]) % (uint64_t)c.T);
-    if (lane + 32 < L) d1 = (int)((idx / src.tpow[lane + 32]) % (uint64_t)c.T);
+    if (idx < 0xffffffffull && src.tpow[0] < 0xffffffffull) {  // 32-bit division is much cheaper
+      const uint32_t i32 = (uint32_t)idx, t32 = (uint32_t)c.T;
+      if (lane < L) d0 = (int)((i32 / (uint32_t)src.tpow[lane]) % t32);
+      if (lane + 32 < L) d1 = (int)((i32 / (uint32_t)src.tpow[lane + 32]) % t32);
+    } else {
+      if (lane < L) d0 = (int)((idx / src.tpow[lane]) % (uint64_t)c.T);
+      if (lane + 32 < L) d1 = (int)((idx / src.tpow[lane + 32]) % (uint64_t)c.T);
+    }
     rank = idx;
   } else {
     const uint64_t g = src.begin + p;
@@ -185,7 +192,7 @@ __device__ __forceinline__ void write_plan(const InstanceConsts& c, const WarpSm
 
 // ------------------------------------------------------------------ K1 / K2
 
-template <int MAXS, int WARPS, bool ARGMIN, bool FAST>
+template <int MAXS, int WARPS, bool ARGMIN, bool FAST, int SRC>
 __global__ void __launch_bounds__(WARPS * 32)
 eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, uint64_t n,
             Outputs o, Pending pend, int feasible_only, KeyPart* parts) {
@@ -204,7 +211,7 @@ eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
   for (uint64_t p = gw; p < n; p += nw) {
     int d0, d1;
     u128 rank;
-    load_digits(c, src, p, d0, d1, rank);
+    load_digits<SRC>(c, src, p, d0, d1, rank);
     PlanOut r;
     if (FAST) eval_plan_fast<MAXS>(c, tb, w, ss[warp], d0, d1, r);
     else eval_plan_warp<MAXS>(c, tb, w, d0, d1, r);
@@ -343,7 +350,9 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
     if (warp == 0) {
       int d0, d1;
       u128 rank;
-      load_digits(c, src, p, d0, d1, rank);
+      if (src.mode == 0) load_digits<0>(c, src, p, d0, d1, rank);
+      else if (src.mode == 1) load_digits<1>(c, src, p, d0, d1, rank);
+      else load_digits<2>(c, src, p, d0, d1, rank);
       PlanOut r;
       r.ps = 0; r.gap = 0.0;
       double tlo = 0, thi = 0;
@@ -594,6 +603,8 @@ __global__ void stage_table_kernel(const InstanceConsts c, RawTables raw, StageE
   e.f_alpha = (float)e.alpha;
   e.f_beta = (float)e.beta;
   e.pad0 = e.pad1 = 0;
+  e.rwo = (e.oct != 0) ? 1.0 / e.oct : 0.0;
+  e.rwd = (e.odt != 0) ? 1.0 / e.odt : 0.0;
   out[idx] = e;
 }
 
@@ -674,28 +685,37 @@ struct HpsInstance {
 
 namespace {
 
-template <int MAXS, int WARPS, bool ARGMIN, bool FAST>
+template <int MAXS, int WARPS, bool ARGMIN, bool FAST, int SRC>
 int launch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
                 int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
   const size_t smem = sizeof(WarpSmem<MAXS>) * WARPS + (FAST ? sizeof(SweepSmem<MAXS>) * WARPS : 0);
-  auto kern = eval_kernel<MAXS, WARPS, ARGMIN, FAST>;
+  auto kern = eval_kernel<MAXS, WARPS, ARGMIN, FAST, SRC>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<grid, WARPS * 32, smem, st>>>(in->c, in->tb, src, n, o, pend, feasible_only, parts);
   CUDA_TRY(cudaGetLastError());
   return HPS_OK;
 }
 
+template <int MAXS, int WARPS, bool ARGMIN, bool FAST>
+int launch_src(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
+               int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
+  if (src.mode == 0) return launch_eval<MAXS, WARPS, ARGMIN, FAST, 0>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (!ARGMIN) return set_err(HPS_E_INVALID_ARG, "per-plan outputs need an explicit plan batch");
+  if (src.mode == 1) return launch_eval<MAXS, WARPS, ARGMIN, FAST, 1>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  return launch_eval<MAXS, WARPS, ARGMIN, FAST, 2>(in, src, n, o, pend, feasible_only, parts, grid, st);
+}
+
 template <bool ARGMIN>
 int dispatch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
                   int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
   if (in->fast) {
-    if (in->c.L <= 16) return launch_eval<16, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
-    if (in->c.L <= 32) return launch_eval<32, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
-    return launch_eval<64, 2, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+    if (in->c.L <= 16) return launch_src<16, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+    if (in->c.L <= 32) return launch_src<32, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+    return launch_src<64, 2, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
   }
-  if (in->c.L <= 16) return launch_eval<16, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
-  if (in->c.L <= 32) return launch_eval<32, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
-  return launch_eval<64, 2, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (in->c.L <= 16) return launch_src<16, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (in->c.L <= 32) return launch_src<32, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  return launch_src<64, 2, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
 }
 
 int warps_per_block(const HpsInstance* in) { return (in->c.L <= 32) ? 4 : 2; }
@@ -986,7 +1006,7 @@ __global__ void gen_plans_kernel(const InstanceConsts c, const PlanSource src, u
   for (uint64_t p = gw; p < n; p += nw) {
     int d0, d1;
     u128 rank;
-    load_digits(c, src, p, d0, d1, rank);
+    load_digits<2>(c, src, p, d0, d1, rank);
     if (lane < c.L) out[p * c.L + lane] = (uint8_t)d0;
     if (lane + 32 < c.L) out[p * c.L + lane + 32] = (uint8_t)d1;
   }

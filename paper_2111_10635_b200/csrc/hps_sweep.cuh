@@ -12,151 +12,114 @@
 //    count(b) and count(a). Once every unpinned stage is within one step, quota_ok on (a, b)
 //    switches at one of the thresholds theta_r(count(b)); that switch point tau* is found
 //    exactly and the remaining bisection steps are comparisons mid >= tau*.
-//  * _best_candidate (ls/provisioner.py:262-314): lanes own tau-intervals (quantiles of a
-//    warp-sorted sample of 32 candidates); each lane merges every leader stage's breakpoint
-//    stream inside its interval in increasing tau, so each threshold is crossed once, keeps
-//    every stage's exact count and next threshold, and per candidate does the reference's
-//    exact sequential per_second sum and cost division.
+//  * _best_candidate (ls/provisioner.py:262-314): candidates are spread round-robin over the
+//    lanes; each unpinned stage's count at a candidate is a CERTIFIED arithmetic count
+//    (reciprocal + rigorous error bound, count_cert) with the exact table search as fallback;
+//    pinned stages (count(tau_hi) == count(tau_lo)) cost nothing; per_second is the reference's
+//    exact sequential sum and the cost the reference's two divisions.
 #pragma once
 #include "hps_eval.cuh"
 
 namespace hps {
 
+constexpr int kTopK = 3;
+
 template <int MAXS>
-struct SweepSmem {   // per-warp state of the fast path, next to WarpSmem
-  double pr[MAXS];               // price per second of stage r's type
-  double nt[MAXS][kWarp];        // per lane: tau at which stage r's count drops next
-  double hd[MAXS][kWarp];        // per lane: tau of stage r's next breakpoint candidate (+inf: none)
-  uint16_t kk[MAXS][kWarp];      // per lane: stage r's count at the lane's current tau
-  uint16_t mp[MAXS][kWarp];      // per lane: count m whose breakpoint is hd[r]
-  // counts fit 16 bits: the fast path is only enabled when every quota <= 16384
+struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase (broadcast reads)
+  double pr[MAXS];   // price per second of stage r's type
+  double etp[MAXS];  // exact et at the pinned count (kmin == kmax), else unused
+  double pmin_rest;  // sum of price*kmin over the stages outside the top-K set
+  double ep_max;     // max over pinned stages of their exact et
+  int32_t top[kTopK];  // unpinned stages with the largest price*(kmax-kmin) (-1: none)
+  int32_t ntop;
 };
 
-// tau of candidate index i of the implicit list {tau_lo, tau_hi, leaders' breakpoints}
+// exact count of stage r at tau in [tau_lo, tau_hi]: certified arithmetic, exact table fallback
 template <int MAXS>
-__device__ __forceinline__ double candidate_tau(const InstanceConsts& c, const DeviceTables& tb,
-                                                const WarpSmem<MAXS>& w, int S, int i,
-                                                double tau_lo, double tau_hi) {
-  if (i == 0) return tau_lo;
-  if (i == 1) return tau_hi;
-  const int j = i - 2;
-  int s = 0;
-  while (w.pre[s + 1] <= j) s++;
-  const double m = w.kmin[s] + (double)(j - w.pre[s]);
-  return te_row(c, tb, w.st[s].type, w.ent[s])[(int)m - 1].et;
+__device__ __noinline__ int count_in_range(const InstanceConsts& c, const DeviceTables& tb,
+                                              const WarpSmem<MAXS>& w, int r, double tau) {
+  const StageEntry& st = w.st[r];
+  const int k = count_cert(st, tau, c.bo);
+  if (k > 0) return k;
+  const TEPair* row = te_row(c, tb, st.type, w.ent[r]);
+  return count_tab(row, tau, (int)w.kmin[r], (int)w.kmax[r], est_count(st, tau));
 }
 
-// Visit the candidates with tau in this lane's interval [b_lo, b_hi), in increasing tau (a merge
-// of every leader stage's breakpoint stream), maintaining every stage's exact count.
-// MODE 0: feed the tie buffer. MODE 1: return the largest tau with cost <= lim.
-template <int MAXS, int MODE>
-__device__ double sweep_lane(const InstanceConsts& c, const DeviceTables& tb, const WarpSmem<MAXS>& w,
-                             SweepSmem<MAXS>& sw, int S, double tau_lo, double tau_hi,
-                             double b_lo, double b_hi, TieBuf& buf, double lim) {
-  const int lane = threadIdx.x & 31;
+// Rigorous lower bound on the cost of candidate tau from stage s (count m): exact counts for s
+// and the top-K stages, count(tau_hi) for the rest; E >= their et, P >= their price sum.
+template <int MAXS>
+__device__ __noinline__ double cost_lower_bound(const InstanceConsts& c, const DeviceTables& tb,
+                                                   const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
+                                                   int s, double tau) {
+  double E = sw.ep_max, P = sw.pmin_rest;
+  bool s_in_top = false;
+  for (int q = 0; q < sw.ntop; q++) {
+    const int r = sw.top[q];
+    s_in_top |= (r == s);
+    const int k = count_in_range<MAXS>(c, tb, w, r, tau);
+    P += sw.pr[r] * (double)k;
+    E = fmax(E, et_approx(w.st[r], (double)k));
+  }
+  if (s >= 0 && !s_in_top && w.kmax[s] != w.kmin[s]) {
+    const int k = count_in_range<MAXS>(c, tb, w, s, tau);
+    P += sw.pr[s] * ((double)k - w.kmin[s]);
+    E = fmax(E, et_approx(w.st[s], (double)k));
+  }
+  // cost_ref = fl(fl(work / fl(batch / E)) * P_seq) >= (work/batch) E P (1 - (2S + 16) u)
+  return c.work / c.batch * E * P * (1.0 - 1e-13);
+}
+
+// cost of candidate tau (numpy column of _best_candidate, ls/provisioner.py:286-308): exact
+// counts, exact sequential per_second, exact E = max_r et_r(k_r) (approximate et values pick the
+// maximiser; every stage within the approximation band is resolved exactly from the TE table).
+template <int MAXS>
+__device__ __noinline__ double cost_fast(const InstanceConsts& c, const DeviceTables& tb,
+                                            const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
+                                            int S, double tau) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double best_tau = -inf;
-  // heads: for each leader stage, the largest m in [kmin, kmax] with et(m) >= b_lo
-  double first = inf;
-  int fs = -1;
+  double P = 0.0, best = -1.0, second = -1.0;
+  int kb = 0, rb = -1;
   for (int r = 0; r < S; r++) {
-    double h = inf;
-    int mm = 0;
-    const int lo = (int)w.kmin[r], hi = (int)w.kmax[r];
-    if (w.pre[r + 1] > w.pre[r]) {  // a class leader whose breakpoints are candidates
-      const TEPair* row = te_row(c, tb, w.st[r].type, w.ent[r]);
-      const double x = fmax(b_lo, tau_lo);
-      if (row[lo - 1].et >= x) {  // some m has et(m) >= x; find the largest (et non-increasing in m)
-        int a = lo, b = hi + 1;   // et(a) >= x, et(b) < x or b out of range
-        while (b - a > 1) { const int md = (a + b) >> 1; if (row[md - 1].et >= x) a = md; else b = md; }
-        const double e = row[a - 1].et;
-        if (e < b_hi && e <= tau_hi) { h = e; mm = a; }
-      }
-    }
-    sw.hd[r][lane] = h;
-    sw.mp[r][lane] = (uint16_t)mm;
-    if (h < first) { first = h; fs = r; }
-  }
-  const bool has_lo = (tau_lo >= b_lo && tau_lo < b_hi);
-  const bool has_hi = (tau_hi >= b_lo && tau_hi < b_hi);
-  double tau = has_lo ? tau_lo : first;
-  if (!(tau < inf) && !has_hi) return best_tau;
-  if (!(tau < inf)) tau = tau_hi;
-  if (!has_lo && fs >= 0) {  // the first candidate is stage fs's head: consume it
-    const TEPair* row = te_row(c, tb, w.st[fs].type, w.ent[fs]);
-    const int m = sw.mp[fs][lane] - 1;
-    double h = inf;
-    if (m >= (int)w.kmin[fs]) {
-      const double e = row[m - 1].et;
-      if (e < b_hi && e <= tau_hi) h = e;
-    }
-    sw.hd[fs][lane] = h;
-    sw.mp[fs][lane] = (uint16_t)m;
-  }
-  // state at the first candidate
-  double E = 0.0;
-  for (int r = 0; r < S; r++) {
-    const StageEntry& st = w.st[r];
-    const TEPair* row = te_row(c, tb, st.type, w.ent[r]);
-    const int lo = (int)w.kmin[r], hi = (int)w.kmax[r];
-    const int k = count_tab(row, tau, lo, hi, est_count(st, tau));
-    const TEPair p = row[k - 1];
-    sw.kk[r][lane] = (uint16_t)k;
-    sw.nt[r][lane] = (k > lo) ? p.th : inf;
-    E = (r == 0) ? p.et : fmax(E, p.et);
-  }
-  bool did_hi = false;
-  for (;;) {
-    // evaluate the current tau: advance crossed stages, exact sequential per_second
-    double P = 0.0, nxt = inf;
-    int ns = -1;
-    for (int r = 0; r < S; r++) {
-      int k = sw.kk[r][lane];
-      if (tau >= sw.nt[r][lane]) {
-        const StageEntry& st = w.st[r];
-        const TEPair* row = te_row(c, tb, st.type, w.ent[r]);
-        const int lo = (int)w.kmin[r];
-        // one step down is the common case: count == k-1 iff tau < theta(k-2)
-        TEPair p = row[k - 2];  // {et(k-1), theta(k-2)}
-        if (k - 1 > lo && tau >= p.th) {
-          k = count_tab(row, tau, lo, k - 2, est_count(st, tau));
-          p = row[k - 1];
-        } else {
-          k = k - 1;
-        }
-        sw.kk[r][lane] = (uint16_t)k;
-        sw.nt[r][lane] = (k > lo) ? p.th : inf;
-        E = fmax(E, p.et);
-      }
-      const double term = sw.pr[r] * (double)k;
-      P = (r == 0) ? term : P + term;
-      const double h = sw.hd[r][lane];
-      if (h < nxt) { nxt = h; ns = r; }
-    }
-    const double thr = (E > 0) ? c.batch / E : inf;
-    const double cost = (thr > c.limit) ? c.work / thr * P : inf;
-    if (MODE == 0) buf.insert(cost, tau); else if (cost <= lim && tau > best_tau) best_tau = tau;
-    if (tau == tau_hi && has_hi) did_hi = true;
-    // next candidate: pop the smallest head (a tau equal to the current one is re-evaluated
-    // harmlessly: same state, same cost)
-    if (ns >= 0 && nxt < inf) {
-      const TEPair* row = te_row(c, tb, w.st[ns].type, w.ent[ns]);
-      const int m = sw.mp[ns][lane] - 1;
-      double h = inf;
-      if (m >= (int)w.kmin[ns]) {
-        const double e = row[m - 1].et;
-        if (e < b_hi && e <= tau_hi) h = e;
-      }
-      sw.hd[ns][lane] = h;
-      sw.mp[ns][lane] = (uint16_t)m;
-      tau = fmax(tau, nxt);
-    } else if (has_hi && !did_hi) {
-      tau = tau_hi;
+    const double kmin = w.kmin[r];
+    double k, ea;
+    if (w.kmax[r] == kmin) {
+      k = kmin;
+      ea = sw.etp[r];
     } else {
-      break;
+      k = (double)count_in_range<MAXS>(c, tb, w, r, tau);
+      ea = et_approx(w.st[r], k);
     }
+    if (ea > best) { second = best; best = ea; rb = r; kb = (int)k; }
+    else if (ea > second) second = ea;
+    const double term = sw.pr[r] * k;
+    P = (r == 0) ? term : P + term;
   }
-  return best_tau;
+  double E;
+  if (second >= best * (1.0 - 1e-14)) {  // near-tie between stages: resolve all candidates
+    E = 0.0;
+    for (int r = 0; r < S; r++) {
+      double k = w.kmin[r];
+      if (w.kmax[r] != k) k = (double)count_in_range<MAXS>(c, tb, w, r, tau);
+      E = fmax(E, te_row(c, tb, w.st[r].type, w.ent[r])[(int)k - 1].et);
+    }
+  } else {
+    E = (w.kmax[rb] == w.kmin[rb]) ? sw.etp[rb] : te_row(c, tb, w.st[rb].type, w.ent[rb])[kb - 1].et;
+  }
+  const double thr = (E > 0) ? c.batch / E : inf;
+  if (!(thr > c.limit)) return inf;
+  return c.work / thr * P;
+}
+
+template <int MAXS>
+__device__ __forceinline__ double cand_tau(const InstanceConsts& c, const DeviceTables& tb,
+                                           const WarpSmem<MAXS>& w, int i, double tau_lo,
+                                           double tau_hi, int& sp, int& s_out) {
+  if (i < 2) { s_out = -1; return (i == 0) ? tau_lo : tau_hi; }
+  const int j = i - 2;
+  while (w.pre[sp + 1] <= j) sp++;
+  s_out = sp;
+  const int m = (int)w.kmin[sp] + (j - w.pre[sp]);
+  return te_row(c, tb, w.st[sp].type, w.ent[sp])[m - 1].et;
 }
 
 template <int MAXS>
@@ -165,57 +128,81 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
                                         double tau_lo, double tau_hi, int n_cand) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  for (int r = lane; r < S; r += 32) sw.pr[r] = c.price_s[w.st[r].type];
-  // lane intervals: 128 evenly spaced candidate indices (4 per lane), sorted across the warp
-  // (bitonic over element index e = 4*lane + q), boundaries at every 4th sorted sample
-  double v[4];
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const int e = lane * 4 + q;
-    v[q] = candidate_tau<MAXS>(c, tb, w, S, (int)(((long long)e * n_cand) >> 7), tau_lo, tau_hi);
-    v[q] = fmin(fmax(v[q], tau_lo), tau_hi);
+  for (int r = lane; r < S; r += 32) {
+    sw.pr[r] = c.price_s[w.st[r].type];
+    sw.etp[r] = (w.kmax[r] == w.kmin[r])
+                    ? te_row(c, tb, w.st[r].type, w.ent[r])[(int)w.kmin[r] - 1].et : 0.0;
   }
-#pragma unroll
-  for (int k = 2; k <= 128; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= 4) {  // partner in lane ^ (j/4), same q
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const int e = lane * 4 + q;
-          const double o = __shfl_xor_sync(0xffffffffu, v[q], j >> 2);
-          const bool up = (e & k) == 0, lower = (e & j) == 0;
-          v[q] = (lower == up) ? fmin(v[q], o) : fmax(v[q], o);
-        }
-      } else {  // partner inside the lane
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          if ((q & j) == 0) {
-            const int e = lane * 4 + q;
-            const bool up = (e & k) == 0;
-            const double a = v[q], b = v[q | j];
-            v[q] = up ? fmin(a, b) : fmax(a, b);
-            v[q | j] = up ? fmax(a, b) : fmin(a, b);
-          }
-        }
-      }
+  __syncwarp();
+  if (lane == 0) {  // top-K unpinned stages by price-weighted count span, and the rest's floor
+    int top[kTopK];
+    double wt[kTopK];
+    int nt = 0;
+    double ep = 0.0;
+    for (int r = 0; r < S; r++) {
+      if (w.kmax[r] == w.kmin[r]) { ep = fmax(ep, sw.etp[r]); continue; }
+      const double v = sw.pr[r] * (w.kmax[r] - w.kmin[r]);
+      int pos = nt < kTopK ? nt : kTopK;
+      while (pos > 0 && wt[pos - 1] < v) { if (pos < kTopK) { wt[pos] = wt[pos - 1]; top[pos] = top[pos - 1]; } pos--; }
+      if (pos < kTopK) { wt[pos] = v; top[pos] = r; if (nt < kTopK) nt++; }
     }
+    double pm = 0.0;
+    for (int r = 0; r < S; r++) {
+      bool in = false;
+      for (int q = 0; q < nt; q++) in |= (top[q] == r);
+      if (!in) pm += sw.pr[r] * w.kmin[r];
+    }
+    for (int q = 0; q < kTopK; q++) sw.top[q] = q < nt ? top[q] : -1;
+    sw.ntop = nt;
+    sw.pmin_rest = pm * (1.0 - 1e-13);
+    sw.ep_max = ep;
   }
-  const double nb = __shfl_down_sync(0xffffffffu, v[0], 1);
-  const double b_lo = (lane == 0) ? -inf : v[0];
-  const double b_hi = (lane == 31) ? inf : nb;
   __syncwarp();
   TieBuf buf;
   buf.init();
-  sweep_lane<MAXS, 0>(c, tb, w, sw, S, tau_lo, tau_hi, b_lo, b_hi, buf, 0.0);
+  const int rounds = (n_cand + 31) >> 5;
+  // warm start: every 8th round of candidates, exactly
+  int sp = 0, s_of;
+  for (int jr = 0; jr < rounds; jr += 8) {
+    const int i = jr * 32 + lane;
+    if (i >= n_cand) continue;
+    const double tau = cand_tau<MAXS>(c, tb, w, i, tau_lo, tau_hi, sp, s_of);
+    if (!(tau >= tau_lo && tau <= tau_hi)) continue;
+    buf.insert(cost_fast<MAXS>(c, tb, w, sw, S, tau), tau);
+  }
+  double ub = warp_min(buf.mn);
+  // remaining candidates: full evaluation only when the lower bound can reach ub + 1e-15
+  sp = 0;
+  for (int jr = 0; jr < rounds; jr++) {
+    if ((jr & 7) == 0) continue;
+    const int i = jr * 32 + lane;
+    if (i < n_cand) {
+      const double tau = cand_tau<MAXS>(c, tb, w, i, tau_lo, tau_hi, sp, s_of);
+      if (tau >= tau_lo && tau <= tau_hi) {
+        const double lim = ub + 1e-15;
+        if (!(cost_lower_bound<MAXS>(c, tb, w, sw, s_of, tau) > lim))
+          buf.insert(cost_fast<MAXS>(c, tb, w, sw, S, tau), tau);
+      }
+    }
+    ub = fmin(ub, warp_min(buf.mn));
+  }
   const double mf = warp_min(buf.mn);
   if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
   const double lim = mf + 1e-15;
   double bt;
-  if (__any_sync(0xffffffffu, buf.overflow))
-    bt = sweep_lane<MAXS, 1>(c, tb, w, sw, S, tau_lo, tau_hi, b_lo, b_hi, buf, lim);
-  else
+  if (__any_sync(0xffffffffu, buf.overflow)) {  // rare: exact second pass with the final limit
+    bt = -inf;
+    sp = 0;
+    for (int i = lane; i < n_cand; i += 32) {
+      const double tau = cand_tau<MAXS>(c, tb, w, i, tau_lo, tau_hi, sp, s_of);
+      if (!(tau >= tau_lo && tau <= tau_hi)) continue;
+      if (tau > bt && !(cost_lower_bound<MAXS>(c, tb, w, sw, s_of, tau) > lim) &&
+          cost_fast<MAXS>(c, tb, w, sw, S, tau) <= lim)
+        bt = tau;
+    }
+  } else {
     bt = buf.best_tau(lim);
+  }
   return warp_max(bt);
 }
 
