@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="plans in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rl", action="store_true", help="skip the cfg4 RL time-to-best measurement")
     return ap.parse_args()
 
 
@@ -266,6 +267,33 @@ def run_ours(args):
     h2d = 4 * T * L * 8 + T * (8 + 8 + 1)  # profile tables + prices/quotas/is_cpu
     d2h = _abi.ARGMIN_NBYTES * world + 8 * 6  # gathered keys + the re-scored winner's outputs
 
+    # ---- RL scheduler, cfg4 (BASELINE configs[3]): 200 rounds x 4096 plans, time-to-best ----
+    rl = None
+    if not args.no_rl:
+        from paper_2111_10635_b200 import load_fixture, policy
+        from paper_2111_10635_b200.model import JobParams
+        g4, c4, lim4 = load_fixture("cfg4")
+        job4 = JobParams(lim4)
+        cfg = policy.TrainerConfig(rounds=200, plans_per_round=4096, seed=0)
+        p0, _ = policy.init_policy(g4, c4, cfg)
+        policy.train(g4, c4, p0, policy.TrainerConfig(rounds=2, plans_per_round=4096, seed=0), job4)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = policy.train(g4, c4, p0, cfg, job4)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        opt = 0.11630007595486111  # brute-force optimum of cfg4 (index 4030)
+        hit = next((i for i, h in enumerate(res.history) if h.best_cost == opt), None)
+        rl = {"workload": "cfg4", "rounds": 200, "plans_per_round": 4096, "wall_s": wall,
+              "rounds_per_s": 200 / wall, "best_cost": res.best.cost,
+              "best_plan": list(res.best.plan.assignment),
+              "time_to_best_s": res.round_wall_s[hit] if hit is not None else None,
+              "round_of_best": hit + 1 if hit is not None else None,
+              "reference_cpu": {"wall_s": 404.3, "time_to_best_s": 15.3,
+                                "source": "SURVEY.md §6 (reference, 1 core, measured in the build container)"}}
+
     if rank == 0:
         peak = fp64_peak(torch, inst.lib, dev)
         kernel_plans_per_s = (hi - lo) / (statistics.median(step_ms) * 1e-3)
@@ -291,6 +319,8 @@ def run_ours(args):
                                  "probe measured in this run (MEASURED_PEAKS.json has no FP64)"},
             "clocks": clocks.summary(),
         }
+        if rl is not None:
+            line["rl"] = rl
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             sample = args.cpu_sample or 80_000 * threads

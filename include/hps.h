@@ -191,6 +191,9 @@ int hps_policy_reinforce(HpsPolicy* policy, const double* d_cost, const uint8_t*
 int hps_policy_state(HpsPolicy* policy, double* state3, int32_t* flags2);
 const char* hps_policy_last_error(void);
 
+/* Device counters of an instrumented build (-DHPS_STATS); HPS_E_CONFIG otherwise. */
+int hps_stats_read(unsigned long long* out, int n, int reset);
+
 /* FP64 pipe microbenchmark (kind 0: dependent-chain DFMA x8 per thread, 16 flops per loop
  * step per chain pair; kind 1: IEEE division). Used for the roofline denominator. */
 int hps_probe_fp64(int kind, double* d_out, int blocks, int threads, int iters, void* stream);

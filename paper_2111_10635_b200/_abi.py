@@ -150,6 +150,7 @@ _SIGNATURES = {
     "hps_policy_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "hps_policy_last_error": (C.c_char_p, []),
     "hps_probe_fp64": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "hps_stats_read": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),
 }
 

@@ -7,9 +7,27 @@
 
 #include "../../include/hps.h"
 
+// HPS_NOINLINE: inlined helpers; HPS_NOINLINE_RARE: one out-of-line copy (rare paths, and hot
+// helpers called from several sites, to keep the hot loops inside the instruction cache)
+#define HPS_NOINLINE __forceinline__
+#define HPS_NOINLINE_RARE __noinline__
+
 namespace hps {
 
 typedef unsigned __int128 u128;
+
+// Optional device counters (build with -DHPS_STATS; see tools/sweep_stats.py)
+enum {
+  ST_PLANS, ST_CHUNKS, ST_CHUNKS_EVAL, ST_CANDS, ST_PROBES_EXACT, ST_PROBES_CLOSED, ST_CERT,
+  ST_CERT_FAIL, ST_TAB, ST_PENDING, ST_STAGES, ST_UNPINNED, ST_NCAND, ST_PLANS_FAST,
+  ST_CYC_A, ST_CYC_B, ST_CYC_C, ST_CYC_P1, ST_CYC_P2, ST_NSTAT
+};
+#ifdef HPS_STATS
+__device__ unsigned long long g_stats[24];
+#define HPS_STAT(i, v) atomicAdd(&hps::g_stats[i], (unsigned long long)(v))
+#else
+#define HPS_STAT(i, v) ((void)0)
+#endif
 
 constexpr int kMaxL = HPS_MAX_LAYERS;
 constexpr int kMaxT = HPS_MAX_TYPES;
@@ -52,7 +70,7 @@ __device__ __forceinline__ double rcp_refined(double x) {
   return fma(r, e, r);
 }
 
-static __device__ __noinline__ int count_cert(const StageEntry& s, double tau, double bo) {
+static __device__ HPS_NOINLINE_RARE int count_cert(const StageEntry& s, double tau, double bo) {
   const double A = tau * bo;  // identical to the reference's first product
   double lo = 1.0, hi = 1.0;
 #pragma unroll
@@ -78,7 +96,8 @@ static __device__ __noinline__ int count_cert(const StageEntry& s, double tau, d
     hi = fmax(hi, q + dq);
   }
   const double c_lo = ceil(lo - 1e-9), c_hi = ceil(hi - 1e-9);
-  if (c_lo != c_hi || !(c_hi < 2.0e9)) return -1;
+  HPS_STAT(ST_CERT, 1);
+  if (c_lo != c_hi || !(c_hi < 2.0e9)) { HPS_STAT(ST_CERT_FAIL, 1); return -1; }
   return c_lo < 1.0 ? 1 : (int)c_lo;
 }
 
@@ -222,7 +241,7 @@ __device__ __forceinline__ u128 dbl_to_u128(double x) {
 }
 
 // Python int/int true division (correctly rounded), 0 <= n < 2^127, d > 0.
-static __device__ __noinline__ double int_true_div(u128 n, int64_t d) {
+static __device__ HPS_NOINLINE_RARE double int_true_div(u128 n, int64_t d) {
   if (n < ((u128)1 << 53)) return (double)(uint64_t)n / (double)d;
   u128 q = n / (u128)d, r = n % (u128)d;
   int e = 0;

@@ -34,6 +34,7 @@ struct WarpSmem {
   int32_t cls[MAXS];   // ET-equivalence class of the entry
   int32_t pre[MAXS + 1];  // exclusive prefix of candidate counts over class leaders
   unsigned long long tsum[kMaxT];
+  const TEPair* row[MAXS];  // TE row of stage r's entry (fast path)
 };
 
 struct PlanOut {
@@ -49,7 +50,7 @@ struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min
   bool overflow;
   double mn;
   __device__ __forceinline__ void init() { n = 0; overflow = false; mn = __longlong_as_double(0x7ff0000000000000LL); }
-  __device__ __noinline__ void insert(double cost, double tau) {
+  __device__ HPS_NOINLINE void insert(double cost, double tau) {
     if (!(cost <= mn + 1e-15) && n > 0) return;  // cannot be within 1e-15 of the minimum
     if (cost < mn) {
       mn = cost;
@@ -114,8 +115,9 @@ __device__ __forceinline__ int est_count(const StageEntry& s, double tau) {
 }
 
 // Exact count(tau) given count(tau) in [lo, hi] (hi <= table cap). row[c].th = theta(c).
-static __device__ __noinline__ int count_tab(const TEPair* row, double tau, int lo, int hi, int g) {
+static __device__ HPS_NOINLINE_RARE int count_tab(const TEPair* row, double tau, int lo, int hi, int g) {
   if (lo >= hi) return lo;
+  HPS_STAT(ST_TAB, 1);
   const int m = min(max(g, lo), hi);
   if (row[m].th <= tau) {  // count <= m: gallop down
     int hb = m, lb, step = 1;
@@ -155,7 +157,7 @@ __device__ __forceinline__ bool quota_sums_ok(const InstanceConsts& c, unsigned 
 
 // Bisection on quota_ok (ls/provisioner.py:430-437). Inputs: counts at tau_hi in kb[] (finite,
 // quota-feasible). Output: tau_lo and the counts at tau_lo.
-static __device__ __noinline__ double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, const StageEntry* st,
+static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, const StageEntry* st,
                               const int32_t* ent, int S, double a, double b, const double kb_in[2],
                               int kb_out[2]) {
   const int lane = threadIdx.x & 31;
@@ -181,6 +183,7 @@ static __device__ __noinline__ double bisect_fast(const InstanceConsts& c, const
     const bool wide = (ub[0] - lb[0] > 1 && ub[0] != kOver) || (ub[1] - lb[1] > 1 && ub[1] != kOver) ||
                       (ub[0] == kOver && lb[0] < Q[0]) || (ub[1] == kOver && lb[1] < Q[1]);
     if (!__any_sync(0xffffffffu, wide)) break;
+    if (lane == 0) HPS_STAT(ST_PROBES_EXACT, 1);
     const double mid = (a + b) / 2.0;
     int km[2];
     bool over = false;
@@ -234,6 +237,7 @@ static __device__ __noinline__ double bisect_fast(const InstanceConsts& c, const
       if (okx) { tstar = x; break; }
       lo_bound = x;
     }
+    if (lane == 0) HPS_STAT(ST_PROBES_CLOSED, 60 - it);
     for (; it < 60; it++) {
       const double mid = (a + b) / 2.0;
       if (mid >= tstar) b = mid; else a = mid;
@@ -249,14 +253,17 @@ static __device__ __noinline__ double bisect_fast(const InstanceConsts& c, const
 
 // Evaluate one candidate tau: numpy _best_candidate column (ls/provisioner.py:286-308).
 // Returns +inf when the column is not ok (throughput <= limit).
-template <int MAXS>
+template <int MAXS, bool CERT = false>
 __device__ __forceinline__ double candidate_cost(const InstanceConsts& c, const DeviceTables& tb,
                                                  const WarpSmem<MAXS>& w, int S, double tau) {
   double E = 0.0, P = 0.0;
   for (int r = 0; r < S; r++) {
     const StageEntry& s = w.st[r];
     double k = w.kmin[r];
-    if (w.kmax[r] != k) k = count_at(s, tau, c.bo);
+    if (w.kmax[r] != k) {
+      const int kc = CERT ? count_cert(s, tau, c.bo) : -1;
+      k = (kc > 0) ? (double)kc : count_at(s, tau, c.bo);
+    }
     double et = et_lookup(c, tb, s, w.ent[r], k);
     double term = c.price_s[s.type] * k;
     if (r == 0) { E = et; P = term; } else { E = fmax(E, et); P = P + term; }
@@ -311,6 +318,7 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
       const int e = entry_index(c.P, type, first, last);
       w.st[s] = tb.stages[e];
       w.ent[s] = e;
+      w.row[s] = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
       invalid |= (w.st[s].valid == 0);
     }
   }
@@ -461,7 +469,7 @@ namespace hps {
 // Phase B: _best_candidate over the implicit candidate set {tau_lo, tau_hi} U breakpoints of
 // class leaders (ls/provisioner.py:442-455, 262-314). Returns the chosen tau, or NaN when no
 // candidate is feasible (InfeasibleError(gap=1.0), ls/provisioner.py:473-477).
-template <int MAXS>
+template <int MAXS, bool CERT = false>
 __device__ double phase_candidates(const InstanceConsts& c, const DeviceTables& tb,
                                    const WarpSmem<MAXS>& w, int S, double tau_lo, double tau_hi,
                                    int n_cand) {
@@ -481,7 +489,7 @@ __device__ double phase_candidates(const InstanceConsts& c, const DeviceTables& 
       tau = et_lookup(c, tb, w.st[sp], w.ent[sp], m);
       if (!(tau >= tau_lo && tau <= tau_hi)) continue;
     }
-    buf.insert(candidate_cost(c, tb, w, S, tau), tau);
+    buf.insert(candidate_cost<MAXS, CERT>(c, tb, w, S, tau), tau);
   }
   const double mf = warp_min(buf.mn);
   if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
@@ -500,7 +508,7 @@ __device__ double phase_candidates(const InstanceConsts& c, const DeviceTables& 
         tau = et_lookup(c, tb, w.st[sp], w.ent[sp], w.kmin[sp] + (double)(j - w.pre[sp]));
         if (!(tau >= tau_lo && tau <= tau_hi)) continue;
       }
-      if (tau > bt && candidate_cost(c, tb, w, S, tau) <= lim) bt = tau;
+      if (tau > bt && candidate_cost<MAXS, CERT>(c, tb, w, S, tau) <= lim) bt = tau;
     }
   } else {
     bt = buf.best_tau(lim);
@@ -583,22 +591,22 @@ __device__ void phase_final(const InstanceConsts& c, const DeviceTables& tb, War
 
 // Whole plan on one warp. Returns with out.status == kStPending when the breakpoint count
 // may exceed 4096 (the block-per-plan slow path then finishes the plan).
-template <int MAXS>
+template <int MAXS, bool HYBRID = false>
 __device__ void eval_plan_warp(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
                                int d0, int d1, PlanOut& out) {
   out.ps = 0;
   out.gap = 0.0;
   double tau_lo, tau_hi;
   int n_cand;
-  if (!phase_stages_bisect<MAXS>(c, tb, w, d0, d1, out, tau_lo, tau_hi, n_cand)) return;
+  if (!phase_stages_bisect<MAXS, HYBRID>(c, tb, w, d0, d1, out, tau_lo, tau_hi, n_cand)) return;
   if (n_cand > kBpLimit) { out.status = kStPending; return; }
-  const double tau = phase_candidates<MAXS>(c, tb, w, out.S, tau_lo, tau_hi, n_cand);
+  const double tau = phase_candidates<MAXS, HYBRID>(c, tb, w, out.S, tau_lo, tau_hi, n_cand);
   if (tau != tau) {
     out.status = HPS_ST_NO_CANDIDATE; out.gap = 1.0;
     out.cost = c.penalty_scale * (1.0 + 1.0);
     return;
   }
-  phase_final<MAXS>(c, tb, w, out.S, tau, out);
+  phase_final<MAXS, HYBRID>(c, tb, w, out.S, tau, out);
 }
 
 }  // namespace hps

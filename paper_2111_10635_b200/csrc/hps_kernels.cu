@@ -193,7 +193,10 @@ __device__ __forceinline__ void write_plan(const InstanceConsts& c, const WarpSm
 // ------------------------------------------------------------------ K1 / K2
 
 template <int MAXS, int WARPS, bool ARGMIN, bool FAST, int SRC>
-__global__ void __launch_bounds__(WARPS * 32)
+#ifndef HPS_MINB
+#define HPS_MINB 24
+#endif
+__global__ void __launch_bounds__(WARPS * 32, HPS_MINB / WARPS)
 eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, uint64_t n,
             Outputs o, Pending pend, int feasible_only, KeyPart* parts) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -213,10 +216,16 @@ eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
     u128 rank;
     load_digits<SRC>(c, src, p, d0, d1, rank);
     PlanOut r;
+#ifdef HPS_HYBRID
+    if (FAST) eval_plan_warp<MAXS, true>(c, tb, w, d0, d1, r);
+#else
     if (FAST) eval_plan_fast<MAXS>(c, tb, w, ss[warp], d0, d1, r);
+#endif
     else eval_plan_warp<MAXS>(c, tb, w, d0, d1, r);
+    if (lane == 0) HPS_STAT(ST_PLANS, 1);
     if (r.status == kStPending) {
       if (lane == 0) {
+        HPS_STAT(ST_PENDING, 1);
         unsigned int at = atomicAdd(pend.count, 1u);
         if (at < pend.cap) pend.list[at] = p;
       }
@@ -1061,6 +1070,21 @@ __global__ void report_kernel(const InstanceConsts c, const DeviceTables tb, con
   feasible[i] = (overall > c.limit) && quota_ok;
 }
 }  // namespace
+
+extern "C" int hps_stats_read(unsigned long long* out, int n, int reset) {
+#ifdef HPS_STATS
+  if (n > 24) n = 24;
+  CUDA_TRY(cudaMemcpyFromSymbol(out, hps::g_stats, sizeof(unsigned long long) * n));
+  if (reset) {
+    unsigned long long z[24] = {0};
+    CUDA_TRY(cudaMemcpyToSymbol(hps::g_stats, z, sizeof(z)));
+  }
+  return HPS_OK;
+#else
+  (void)out; (void)n; (void)reset;
+  return set_err(HPS_E_CONFIG, "built without -DHPS_STATS");
+#endif
+}
 
 extern "C" int hps_random_plans(HpsInstance* in, const HpsPcg64* g, uint64_t first, uint64_t n,
                                 uint8_t* d_plans, void* stream) {

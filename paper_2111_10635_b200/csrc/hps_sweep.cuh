@@ -12,116 +12,95 @@
 //    count(b) and count(a). Once every unpinned stage is within one step, quota_ok on (a, b)
 //    switches at one of the thresholds theta_r(count(b)); that switch point tau* is found
 //    exactly and the remaining bisection steps are comparisons mid >= tau*.
-//  * _best_candidate (ls/provisioner.py:262-314): candidates are spread round-robin over the
-//    lanes; each unpinned stage's count at a candidate is a CERTIFIED arithmetic count
-//    (reciprocal + rigorous error bound, count_cert) with the exact table search as fallback;
-//    pinned stages (count(tau_hi) == count(tau_lo)) cost nothing; per_second is the reference's
-//    exact sequential sum and the cost the reference's two divisions.
+//  * _best_candidate (ls/provisioner.py:262-314): candidates round-robin over lanes; counts are
+//    CERTIFIED arithmetic counts (reciprocal + rigorous error bound, count_cert) with the exact
+//    table search as fallback; a warm start plus a rigorous two-stage lower bound skips the
+//    candidates that cannot reach the minimum or its 1e-15 tie window; evaluated candidates use
+//    the reference's exact sequential per_second sum and its two cost divisions.
 #pragma once
 #include "hps_eval.cuh"
 
 namespace hps {
 
-constexpr int kTopK = 3;
-
 template <int MAXS>
 struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase (broadcast reads)
   double pr[MAXS];   // price per second of stage r's type
   double etp[MAXS];  // exact et at the pinned count (kmin == kmax), else unused
-  double pmin_rest;  // sum of price*kmin over the stages outside the top-K set
+  double pmin_rest;  // sum over non-top stages of price * kmin, rounded down by 1e-13
   double ep_max;     // max over pinned stages of their exact et
-  int32_t top[kTopK];  // unpinned stages with the largest price*(kmax-kmin) (-1: none)
-  int32_t ntop;
+  int32_t top[2];    // unpinned stages with the largest price-weighted count span (-1: none)
+  double q[64];      // survivors of the lower-bound filter, evaluated 32 at a time
 };
 
-// exact count of stage r at tau in [tau_lo, tau_hi]: certified arithmetic, exact table fallback
+// exact count at tau in [tau_lo, tau_hi] (count in [kmin, kmax]): certified, table fallback
 template <int MAXS>
-__device__ __noinline__ int count_in_range(const InstanceConsts& c, const DeviceTables& tb,
-                                              const WarpSmem<MAXS>& w, int r, double tau) {
-  const StageEntry& st = w.st[r];
-  const int k = count_cert(st, tau, c.bo);
+__device__ __forceinline__ int count_fast(double bo, const WarpSmem<MAXS>& w, int r, double tau) {
+  const int k = count_cert(w.st[r], tau, bo);
   if (k > 0) return k;
-  const TEPair* row = te_row(c, tb, st.type, w.ent[r]);
-  return count_tab(row, tau, (int)w.kmin[r], (int)w.kmax[r], est_count(st, tau));
+  return count_tab(w.row[r], tau, (int)w.kmin[r], (int)w.kmax[r], est_count(w.st[r], tau));
 }
 
-// Rigorous lower bound on the cost of candidate tau from stage s (count m): exact counts for s
-// and the top-K stages, count(tau_hi) for the rest; E >= their et, P >= their price sum.
-template <int MAXS>
-__device__ __noinline__ double cost_lower_bound(const InstanceConsts& c, const DeviceTables& tb,
-                                                   const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
-                                                   int s, double tau) {
-  double E = sw.ep_max, P = sw.pmin_rest;
-  bool s_in_top = false;
-  for (int q = 0; q < sw.ntop; q++) {
-    const int r = sw.top[q];
-    s_in_top |= (r == s);
-    const int k = count_in_range<MAXS>(c, tb, w, r, tau);
-    P += sw.pr[r] * (double)k;
-    E = fmax(E, et_approx(w.st[r], (double)k));
-  }
-  if (s >= 0 && !s_in_top && w.kmax[s] != w.kmin[s]) {
-    const int k = count_in_range<MAXS>(c, tb, w, s, tau);
-    P += sw.pr[s] * ((double)k - w.kmin[s]);
-    E = fmax(E, et_approx(w.st[s], (double)k));
-  }
-  // cost_ref = fl(fl(work / fl(batch / E)) * P_seq) >= (work/batch) E P (1 - (2S + 16) u)
-  return c.work / c.batch * E * P * (1.0 - 1e-13);
-}
+struct CostScalars {  // the four job constants the cost needs (no parameter-struct copies)
+  double bo, batch, work, limit;
+};
 
-// cost of candidate tau (numpy column of _best_candidate, ls/provisioner.py:286-308): exact
-// counts, exact sequential per_second, exact E = max_r et_r(k_r) (approximate et values pick the
-// maximiser; every stage within the approximation band is resolved exactly from the TE table).
+// exact cost of candidate tau (numpy column of _best_candidate, ls/provisioner.py:286-308);
+// one out-of-line copy shared by every call site
 template <int MAXS>
-__device__ __noinline__ double cost_fast(const InstanceConsts& c, const DeviceTables& tb,
-                                            const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
-                                            int S, double tau) {
+__device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<MAXS>& w,
+                                          const SweepSmem<MAXS>& sw, int S, double tau) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double P = 0.0, best = -1.0, second = -1.0;
-  int kb = 0, rb = -1;
+  double P = 0.0, E = 0.0;
   for (int r = 0; r < S; r++) {
-    const double kmin = w.kmin[r];
-    double k, ea;
-    if (w.kmax[r] == kmin) {
-      k = kmin;
-      ea = sw.etp[r];
+    double et;
+    int k;
+    if (w.kmax[r] == w.kmin[r]) {
+      k = (int)w.kmin[r];
+      et = sw.etp[r];
     } else {
-      k = (double)count_in_range<MAXS>(c, tb, w, r, tau);
-      ea = et_approx(w.st[r], k);
+      k = count_fast<MAXS>(cs.bo, w, r, tau);
+      et = w.row[r][k - 1].et;
     }
-    if (ea > best) { second = best; best = ea; rb = r; kb = (int)k; }
-    else if (ea > second) second = ea;
-    const double term = sw.pr[r] * k;
+    E = (r == 0) ? et : fmax(E, et);
+    const double term = sw.pr[r] * (double)k;
     P = (r == 0) ? term : P + term;
   }
-  double E;
-  if (second >= best * (1.0 - 1e-14)) {  // near-tie between stages: resolve all candidates
-    E = 0.0;
-    for (int r = 0; r < S; r++) {
-      double k = w.kmin[r];
-      if (w.kmax[r] != k) k = (double)count_in_range<MAXS>(c, tb, w, r, tau);
-      E = fmax(E, te_row(c, tb, w.st[r].type, w.ent[r])[(int)k - 1].et);
-    }
-  } else {
-    E = (w.kmax[rb] == w.kmin[rb]) ? sw.etp[rb] : te_row(c, tb, w.st[rb].type, w.ent[rb])[kb - 1].et;
+  const double thr = (E > 0) ? cs.batch / E : inf;
+  if (!(thr > cs.limit)) return inf;
+  return cs.work / thr * P;
+}
+
+// rigorous lower bound: exact counts of the two top stages, count(tau_hi) for the others
+template <int MAXS>
+__device__ __forceinline__ double cost_bound(const CostScalars cs, const WarpSmem<MAXS>& w,
+                                             const SweepSmem<MAXS>& sw, double tau) {
+  double P = sw.pmin_rest, E = sw.ep_max;
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    const int r = sw.top[q];
+    if (r < 0) continue;
+    const int k = count_fast<MAXS>(cs.bo, w, r, tau);
+    P += sw.pr[r] * (double)k;
+    E = fmax(E, w.row[r][k - 1].et);
   }
-  const double thr = (E > 0) ? c.batch / E : inf;
-  if (!(thr > c.limit)) return inf;
-  return c.work / thr * P;
+  // cost_ref = fl(fl(work / fl(batch / E)) * P_seq) >= (work / batch) E P (1 - 1e-13)
+  return cs.work / cs.batch * E * P * (1.0 - 1e-13);
 }
 
 template <int MAXS>
-__device__ __forceinline__ double cand_tau(const InstanceConsts& c, const DeviceTables& tb,
-                                           const WarpSmem<MAXS>& w, int i, double tau_lo,
-                                           double tau_hi, int& sp, int& s_out) {
-  if (i < 2) { s_out = -1; return (i == 0) ? tau_lo : tau_hi; }
+__device__ __forceinline__ double cand_tau(const WarpSmem<MAXS>& w, int i, int& sp, double tau_lo,
+                                           double tau_hi) {
+  if (i < 2) return (i == 0) ? tau_lo : tau_hi;
   const int j = i - 2;
   while (w.pre[sp + 1] <= j) sp++;
-  s_out = sp;
   const int m = (int)w.kmin[sp] + (j - w.pre[sp]);
-  return te_row(c, tb, w.st[sp].type, w.ent[sp])[m - 1].et;
+  return w.row[sp][m - 1].et;
 }
 
+// _best_candidate: round-robin candidates over lanes. A warm-start pass evaluates every 8th
+// round exactly; the remaining candidates are evaluated exactly only when a rigorous lower bound
+// (two top stages exact) does not exceed the best cost so far + 1e-15. A skipped candidate
+// therefore costs more than the final minimum + 1e-15: it is neither the minimum nor a tie.
 template <int MAXS>
 __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTables& tb,
                                         const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
@@ -130,61 +109,77 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   for (int r = lane; r < S; r += 32) {
     sw.pr[r] = c.price_s[w.st[r].type];
-    sw.etp[r] = (w.kmax[r] == w.kmin[r])
-                    ? te_row(c, tb, w.st[r].type, w.ent[r])[(int)w.kmin[r] - 1].et : 0.0;
+    sw.etp[r] = (w.kmax[r] == w.kmin[r]) ? w.row[r][(int)w.kmin[r] - 1].et : 0.0;
   }
   __syncwarp();
-  if (lane == 0) {  // top-K unpinned stages by price-weighted count span, and the rest's floor
-    int top[kTopK];
-    double wt[kTopK];
-    int nt = 0;
-    double ep = 0.0;
+  if (lane == 0) {
+    int t0 = -1, t1 = -1;
+    double v0 = -1.0, v1 = -1.0, ep = 0.0;
     for (int r = 0; r < S; r++) {
       if (w.kmax[r] == w.kmin[r]) { ep = fmax(ep, sw.etp[r]); continue; }
       const double v = sw.pr[r] * (w.kmax[r] - w.kmin[r]);
-      int pos = nt < kTopK ? nt : kTopK;
-      while (pos > 0 && wt[pos - 1] < v) { if (pos < kTopK) { wt[pos] = wt[pos - 1]; top[pos] = top[pos - 1]; } pos--; }
-      if (pos < kTopK) { wt[pos] = v; top[pos] = r; if (nt < kTopK) nt++; }
+      if (v > v0) { v1 = v0; t1 = t0; v0 = v; t0 = r; }
+      else if (v > v1) { v1 = v; t1 = r; }
     }
     double pm = 0.0;
-    for (int r = 0; r < S; r++) {
-      bool in = false;
-      for (int q = 0; q < nt; q++) in |= (top[q] == r);
-      if (!in) pm += sw.pr[r] * w.kmin[r];
-    }
-    for (int q = 0; q < kTopK; q++) sw.top[q] = q < nt ? top[q] : -1;
-    sw.ntop = nt;
+    for (int r = 0; r < S; r++)
+      if (r != t0 && r != t1) pm += sw.pr[r] * w.kmin[r];
+    sw.top[0] = t0;
+    sw.top[1] = t1;
     sw.pmin_rest = pm * (1.0 - 1e-13);
     sw.ep_max = ep;
+    HPS_STAT(ST_NCAND, n_cand);
+    HPS_STAT(ST_PLANS_FAST, 1);
+    HPS_STAT(ST_STAGES, S);
   }
   __syncwarp();
+  const CostScalars cs{c.bo, c.batch, c.work, c.limit};
   TieBuf buf;
   buf.init();
   const int rounds = (n_cand + 31) >> 5;
-  // warm start: every 8th round of candidates, exactly
-  int sp = 0, s_of;
-  for (int jr = 0; jr < rounds; jr += 8) {
+  int sp = 0;
+  for (int jr = 0; jr < rounds; jr += 8) {  // warm start: every 8th round exactly
     const int i = jr * 32 + lane;
-    if (i >= n_cand) continue;
-    const double tau = cand_tau<MAXS>(c, tb, w, i, tau_lo, tau_hi, sp, s_of);
+    if (i >= n_cand) break;
+    const double tau = cand_tau<MAXS>(w, i, sp, tau_lo, tau_hi);
     if (!(tau >= tau_lo && tau <= tau_hi)) continue;
-    buf.insert(cost_fast<MAXS>(c, tb, w, sw, S, tau), tau);
+    HPS_STAT(ST_CANDS, 1);
+    buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau), tau);
   }
   double ub = warp_min(buf.mn);
-  // remaining candidates: full evaluation only when the lower bound can reach ub + 1e-15
+  // the other rounds: lower-bound filter; survivors are compacted into sw.q and evaluated
+  // densely (a warp only saves work when all 32 lanes skip, so skipping must be compacted)
   sp = 0;
+  int qn = 0;
+  const unsigned lt = (1u << lane) - 1u;
   for (int jr = 0; jr < rounds; jr++) {
     if ((jr & 7) == 0) continue;
     const int i = jr * 32 + lane;
+    bool keep = false;
+    double tau = 0.0;
     if (i < n_cand) {
-      const double tau = cand_tau<MAXS>(c, tb, w, i, tau_lo, tau_hi, sp, s_of);
-      if (tau >= tau_lo && tau <= tau_hi) {
-        const double lim = ub + 1e-15;
-        if (!(cost_lower_bound<MAXS>(c, tb, w, sw, s_of, tau) > lim))
-          buf.insert(cost_fast<MAXS>(c, tb, w, sw, S, tau), tau);
-      }
+      tau = cand_tau<MAXS>(w, i, sp, tau_lo, tau_hi);
+      keep = tau >= tau_lo && tau <= tau_hi && !(cost_bound<MAXS>(cs, w, sw, tau) > ub + 1e-15);
     }
-    ub = fmin(ub, warp_min(buf.mn));
+    const unsigned mk = __ballot_sync(0xffffffffu, keep);
+    if (keep) sw.q[qn + __popc(mk & lt)] = tau;
+    qn += __popc(mk);
+    __syncwarp();
+    if (qn >= 32) {
+      const double t = sw.q[qn - 32 + lane];
+      HPS_STAT(ST_CANDS, 1);
+      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t), t);
+      qn -= 32;
+      ub = fmin(ub, warp_min(buf.mn));
+      __syncwarp();
+    }
+  }
+  if (qn > 0) {
+    if (lane < qn) {
+      const double t = sw.q[lane];
+      HPS_STAT(ST_CANDS, 1);
+      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t), t);
+    }
   }
   const double mf = warp_min(buf.mn);
   if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
@@ -194,11 +189,9 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     bt = -inf;
     sp = 0;
     for (int i = lane; i < n_cand; i += 32) {
-      const double tau = cand_tau<MAXS>(c, tb, w, i, tau_lo, tau_hi, sp, s_of);
-      if (!(tau >= tau_lo && tau <= tau_hi)) continue;
-      if (tau > bt && !(cost_lower_bound<MAXS>(c, tb, w, sw, s_of, tau) > lim) &&
-          cost_fast<MAXS>(c, tb, w, sw, S, tau) <= lim)
-        bt = tau;
+      const double tau = cand_tau<MAXS>(w, i, sp, tau_lo, tau_hi);
+      if (!(tau >= tau_lo && tau <= tau_hi) || !(tau > bt)) continue;
+      if (!(cost_bound<MAXS>(cs, w, sw, tau) > lim) && cost_exact<MAXS>(cs, w, sw, S, tau) <= lim) bt = tau;
     }
   } else {
     bt = buf.best_tau(lim);
@@ -214,15 +207,31 @@ __device__ void eval_plan_fast(const InstanceConsts& c, const DeviceTables& tb, 
   out.gap = 0.0;
   double tau_lo, tau_hi;
   int n_cand;
+#ifdef HPS_STATS
+  const long long t0 = clock64();
+#endif
   if (!phase_stages_bisect<MAXS, true>(c, tb, w, d0, d1, out, tau_lo, tau_hi, n_cand)) return;
   if (n_cand > kBpLimit) { out.status = kStPending; return; }
+#ifdef HPS_STATS
+  const long long t1 = clock64();
+#endif
   const double tau = phase_candidates_fast<MAXS>(c, tb, w, sw, out.S, tau_lo, tau_hi, n_cand);
+#ifdef HPS_STATS
+  const long long t2 = clock64();
+  if ((threadIdx.x & 31) == 0) { HPS_STAT(ST_CYC_A, t1 - t0); HPS_STAT(ST_CYC_B, t2 - t1); }
+#endif
   if (tau != tau) {
     out.status = HPS_ST_NO_CANDIDATE; out.gap = 1.0;
     out.cost = c.penalty_scale * (1.0 + 1.0);
     return;
   }
+#ifdef HPS_STATS
+  const long long t3 = clock64();
+#endif
   phase_final<MAXS, true>(c, tb, w, out.S, tau, out);
+#ifdef HPS_STATS
+  if ((threadIdx.x & 31) == 0) HPS_STAT(ST_CYC_C, clock64() - t3);
+#endif
 }
 
 }  // namespace hps

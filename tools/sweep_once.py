@@ -19,8 +19,15 @@ def main():
     from paper_2111_10635_b200.model import JobParams
     g, c, limit = load_fixture(a.instance)
     inst = DeviceInstance(g, c, JobParams(limit))
-    for _ in range(a.repeat):
-        key = inst.read_argmin(inst.enum_argmin_async(a.begin, a.begin + a.count, True))
+    import time
+    for r in range(a.repeat):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        buf = inst.enum_argmin_async(a.begin, a.begin + a.count, True)
+        e1.record()
+        key = inst.read_argmin(buf)
+        print(f"sweep {a.count} plans: {e0.elapsed_time(e1):.2f} ms", flush=True)
     torch.cuda.synchronize()
     print(key)
 
