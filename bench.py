@@ -269,24 +269,23 @@ def run_ours(args):
 
     # ---- RL scheduler, cfg4 (BASELINE configs[3]): 200 rounds x 4096 plans, time-to-best ----
     rl = None
-    if not args.no_rl:
+    if not args.no_rl and rank == 0:  # latency-bound per round: timed unsharded on one GPU
         from paper_2111_10635_b200 import load_fixture, policy
         from paper_2111_10635_b200.model import JobParams
         g4, c4, lim4 = load_fixture("cfg4")
         job4 = JobParams(lim4)
         cfg = policy.TrainerConfig(rounds=200, plans_per_round=4096, seed=0)
         p0, _ = policy.init_policy(g4, c4, cfg)
-        policy.train(g4, c4, p0, policy.TrainerConfig(rounds=2, plans_per_round=4096, seed=0), job4)
-        if world > 1:
-            dist.barrier()
+        policy.train(g4, c4, p0, policy.TrainerConfig(rounds=2, plans_per_round=4096, seed=0), job4,
+                     shard=False)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = policy.train(g4, c4, p0, cfg, job4)
+        res = policy.train(g4, c4, p0, cfg, job4, shard=False)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         opt = 0.11630007595486111  # brute-force optimum of cfg4 (index 4030)
         hit = next((i for i, h in enumerate(res.history) if h.best_cost == opt), None)
-        rl = {"workload": "cfg4", "rounds": 200, "plans_per_round": 4096, "wall_s": wall,
+        rl = {"workload": "cfg4", "rounds": 200, "plans_per_round": 4096, "gpus": 1, "wall_s": wall,
               "rounds_per_s": 200 / wall, "best_cost": res.best.cost,
               "best_plan": list(res.best.plan.assignment),
               "time_to_best_s": res.round_wall_s[hit] if hit is not None else None,

@@ -347,11 +347,14 @@ def _dist():
 def train(graph, catalog, params0: PolicyParams, config: TrainerConfig, job,
           provisioner_config: ProvisionerConfig = ProvisionerConfig(),
           score_fn: Callable | None = None, group=None,
-          record_plans: bool = False) -> TrainingResult:
+          record_plans: bool = False, shard: bool = True) -> TrainingResult:
     """REINFORCE training loop (ls/policy/training.py:164-274) with every round on the device.
 
     ``score_fn`` may be any callable like the reference's; a non-device callable is called on
     the host for each sampled plan (the reference semantics), the default is the device scorer.
+    ``shard=False`` keeps the whole round on this rank even when torch.distributed is
+    initialised (a round of a few thousand plans is latency-bound: one GPU is faster than a
+    per-round all_gather).
     """
     import torch
     from .instance import pcg_from_generator
@@ -365,7 +368,7 @@ def train(graph, catalog, params0: PolicyParams, config: TrainerConfig, job,
     inst = device_instance(graph, catalog, job, provisioner_config) if device_scoring else None
     rng = np.random.default_rng([config.seed, 1])
     pcg = pcg_from_generator(rng)
-    dist = _dist()
+    dist = _dist() if shard else None
     rank, world = (dist.get_rank(group), dist.get_world_size(group)) if dist else (0, 1)
     lo, hi = G * rank // world, G * (rank + 1) // world
     plans = torch.empty((G, L), dtype=torch.uint8, device=dev)
