@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="plans in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rl", action="store_true", help="skip the cfg4 RL time-to-best measurement")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 random-plan measurements")
     return ap.parse_args()
 
 
@@ -293,6 +294,44 @@ def run_ours(args):
               "reference_cpu": {"wall_s": 404.3, "time_to_best_s": 15.3,
                                 "source": "SURVEY.md §6 (reference, 1 core, measured in the build container)"}}
 
+    # ---- cfg5 (BASELINE configs[4]): 64 layers x 4 types, random plans of default_rng(0) ----
+    #   batch: hps_score_plans with every plan's outputs (cost, status, gap, ps, k) from a device
+    #          batch of 2^20 plans;  sweep: plans generated in-kernel + fused argmin
+    r5 = None
+    if not args.no_cfg5:
+        from paper_2111_10635_b200 import load_fixture
+        from paper_2111_10635_b200.instance import pcg_from_generator
+        from paper_2111_10635_b200.model import JobParams
+        import numpy as np
+        g5, c5, lim5 = load_fixture("cfg5")
+        inst5 = DeviceInstance(g5, c5, JobParams(lim5))
+        pcg = pcg_from_generator(np.random.default_rng(0))
+        nb = 1 << 20
+        plo, phi = shard_range(0, nb, rank, world)
+        plans5 = inst5.random_plans(pcg, plo, phi - plo)
+        inst5.score(plans5[:4096])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out5 = inst5.score(plans5)
+        e1.record()
+        torch.cuda.synchronize()
+        bms = e0.elapsed_time(e1)
+        e0.record()
+        key5 = inst5.read_argmin(inst5.random_argmin_async(pcg, plo, phi - plo))
+        e1.record()
+        torch.cuda.synchronize()
+        sms = e0.elapsed_time(e1)
+        t5 = torch.tensor([bms, sms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        feas = int(((out5["status"] & 0x7F) == 0).sum().item())
+        r5 = {"workload": "cfg5", "layers": 64, "types": 4, "plans": nb,
+              "batch_plans_per_s": nb / (float(t5[0]) * 1e-3),
+              "sweep_plans_per_s": nb / (float(t5[1]) * 1e-3),
+              "feasible_fraction": feas / (phi - plo),
+              "note": "first 2^20 plans of default_rng(0).integers(0,4,64) per call (ls/baselines.py:270-271)"}
+
     if rank == 0:
         peak = fp64_peak(torch, inst.lib, dev)
         kernel_plans_per_s = (hi - lo) / (statistics.median(step_ms) * 1e-3)
@@ -320,6 +359,8 @@ def run_ours(args):
         }
         if rl is not None:
             line["rl"] = rl
+        if r5 is not None:
+            line["cfg5_random"] = r5
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             sample = args.cpu_sample or 80_000 * threads

@@ -186,6 +186,14 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
     if (lane == 0) HPS_STAT(ST_PROBES_EXACT, 1);
     const double mid = (a + b) / 2.0;
     int km[2];
+    // some stage certainly above its quota (mid < theta(Q)): quota_ok(mid) is false, no counts
+    const bool over0 = (ub[0] == kOver && mid < thq[0]) || (ub[1] == kOver && mid < thq[1]);
+    if (__any_sync(0xffffffffu, over0)) {
+      a = mid;
+      for (int slot = 0; slot < 2; slot++)
+        if (ub[slot] == kOver && mid < thq[slot]) ub[slot] = kOver;  // (unchanged: still over)
+      continue;
+    }
     bool over = false;
     for (int slot = 0; slot < 2; slot++) {
       km[slot] = lb[slot];

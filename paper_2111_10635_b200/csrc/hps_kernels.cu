@@ -249,23 +249,41 @@ eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
 
 // ------------------------------------------------------------------ K7 slow path
 
+// _CostModel.real_cost (ls/provisioner.py:230-249), evaluated by one warp: lanes compute the
+// stages' real counts and times; the per_second sum stays CPython's sequential Neumaier sum in
+// stage order (lane 0), so the value is bit-identical to the reference's.
 __device__ double real_cost_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double tau) {
-  // _CostModel.real_cost (ls/provisioner.py:230-249)
+  const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double ks[kMaxL];
-  for (int s = 0; s < S; s++) {
+  __shared__ double terms[2][64];  // per warp-0 use only (the slow kernel calls it from warp 0)
+  bool raised = false;
+  double et = 0.0;
+  for (int s = lane; s < S; s += 32) {
     double r, g;
-    if (!floor_count(w.st[s], tau, c.bo, r, g)) return inf;
-    ks[s] = pmax(1.0, r);
+    if (!floor_count(w.st[s], tau, c.bo, r, g)) { raised = true; continue; }
+    const double k = pmax(1.0, r);
+    et = fmax(et, stage_et(w.st[s], k));  // max over stages: order-free
+    terms[0][s] = c.price_s[w.st[s].type] * k;
   }
-  double et = stage_et(w.st[0], ks[0]);
-  for (int s = 1; s < S; s++) et = pmax(et, stage_et(w.st[s], ks[s]));
-  if (et <= 0) return 0.0;
-  const double thr = c.batch / et;
-  if (!(thr > c.limit)) return inf;
-  PySum ps;
-  for (int s = 0; s < S; s++) ps.add(c.price_s[w.st[s].type] * ks[s]);
-  return c.work / thr * ps.result();
+  if (__any_sync(0xffffffffu, raised)) return inf;
+  et = warp_max(et);
+  __syncwarp();
+  double out = 0.0;
+  if (lane == 0) {
+    if (et <= 0) {
+      out = 0.0;
+    } else {
+      const double thr = c.batch / et;
+      if (!(thr > c.limit)) {
+        out = inf;
+      } else {
+        PySum ps;
+        for (int s = 0; s < S; s++) ps.add(terms[0][s]);
+        out = c.work / thr * ps.result();
+      }
+    }
+  }
+  return __shfl_sync(0xffffffffu, out, 0);
 }
 
 __device__ bool newton_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double lo, double hi,
@@ -421,10 +439,10 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       bool ovf = false;
       if (nc > (unsigned)kBpLimit) {  // ls/provisioner.py:456-470
         ovf = true;
-        if (tid == 0) {
+        if (warp == 0) {  // sequential search, each real_cost evaluated warp-parallel
           double ts;
           if (!newton_dev(c, w, S, tau_lo, tau_hi, ts)) ts = golden_dev(c, w, S, tau_lo, tau_hi);
-          s_tau_star = ts;
+          if (lane == 0) s_tau_star = ts;
         }
         __syncthreads();
         const double ts = s_tau_star;
@@ -471,7 +489,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       // _best_candidate over the explicit list, all threads
       TieBuf buf;
       buf.init();
-      for (unsigned i = tid; i < nc; i += kSlowThreads) buf.insert(candidate_cost<64>(c, tb, w, S, cand[i]), cand[i]);
+      for (unsigned i = tid; i < nc; i += kSlowThreads) buf.insert(candidate_cost<64, true>(c, tb, w, S, cand[i]), cand[i]);
       red_d[tid] = buf.mn;
       __syncthreads();
       if (tid == 0) for (int i = 1; i < kSlowThreads; i++) red_d[0] = fmin(red_d[0], red_d[i]);
@@ -484,7 +502,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
         const double lim = mf + 1e-15;
         if (any_ovf) {
           for (unsigned i = tid; i < nc; i += kSlowThreads)
-            if (cand[i] > bt && candidate_cost<64>(c, tb, w, S, cand[i]) <= lim) bt = cand[i];
+            if (cand[i] > bt && candidate_cost<64, true>(c, tb, w, S, cand[i]) <= lim) bt = cand[i];
         } else {
           bt = buf.best_tau(lim);
         }
@@ -747,7 +765,7 @@ int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending p
              int feasible_only, KeyPart* slow_parts, cudaStream_t st) {
   const size_t per_block = slow_per_block(in);
   double* scratch = nullptr;
-  const size_t cap_blocks = std::max<size_t>(8, ((size_t)512 << 20) / (per_block * sizeof(double)));
+  const size_t cap_blocks = std::max<size_t>(8, ((size_t)4 << 30) / (per_block * sizeof(double)));
   const int blocks = (int)std::min<size_t>((size_t)in->sm_count * 2, cap_blocks);
   CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
   slow_kernel<<<blocks, kSlowThreads, 0, st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
@@ -842,6 +860,13 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   CUDA_TRY(cudaGetDevice(&dev));
   auto* in = new HpsInstance();
   cudaDeviceGetAttribute(&in->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = 8ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   InstanceConsts& c = in->c;
   memset(&c, 0, sizeof(c));
   c.L = L; c.T = T; c.P = L * (L + 1) / 2;
