@@ -712,6 +712,176 @@ struct HpsInstance {
 
 namespace {
 
+// ------------------------------------------------------------------ split fast path
+// K1a: runs, exits and the quota bisection; finished (infeasible) plans are emitted here, the
+// rest leave a compact state for K1b (candidate phase + final). Two small kernels keep each
+// hot loop inside the instruction cache (one fused kernel stalled on instruction fetch).
+
+template <int MAXS>
+struct PlanState {
+  uint64_t p, rank_hi, rank_lo;
+  double tau_lo, tau_hi;
+  int32_t S, n_cand;
+  int32_t ent[MAXS];
+  int32_t kmin[MAXS], kmax[MAXS];
+  int32_t pre[MAXS + 1];
+};
+
+struct Cont {
+  void* states;
+  unsigned int* count;
+};
+
+__device__ __forceinline__ void merge_part(KeyPart* parts, uint64_t slot, int first, const Key& best,
+                                           unsigned long long feas, uint32_t flags) {
+  KeyPart kp{best, 0ull, feas, flags};
+  if (!first) {
+    const KeyPart o = parts[slot];
+    if (key_less(o.best, kp.best)) kp.best = o.best;
+    kp.feasible += o.feasible;
+    kp.flags |= o.flags;
+  }
+  parts[slot] = kp;
+}
+
+#ifndef HPS_STAGE_MINB
+#define HPS_STAGE_MINB 32
+#endif
+template <int MAXS, int WARPS, bool ARGMIN, int SRC>
+__global__ void __launch_bounds__(WARPS * 32, HPS_STAGE_MINB / WARPS)
+stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, uint64_t p0,
+             uint64_t p1, Outputs o, Pending pend, Cont cont, int feasible_only, KeyPart* parts,
+             int first) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem<MAXS>& w = sm[warp];
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
+  PlanState<MAXS>* states = reinterpret_cast<PlanState<MAXS>*>(cont.states);
+  Key best;
+  best.cost = __longlong_as_double(0x7ff0000000000000LL);
+  best.hi = best.lo = ~0ull;
+  best.status = 0;
+  uint32_t flags = 0;
+  for (uint64_t p = p0 + gw; p < p1; p += nw) {
+    int d0, d1;
+    u128 rank;
+    load_digits<SRC>(c, src, p, d0, d1, rank);
+    PlanOut r;
+    r.ps = 0;
+    r.gap = 0.0;
+    double tau_lo, tau_hi;
+    int n_cand;
+    if (lane == 0) HPS_STAT(ST_PLANS, 1);
+    if (phase_stages_bisect<MAXS, true>(c, tb, w, d0, d1, r, tau_lo, tau_hi, n_cand)) {
+      if (n_cand > kBpLimit) {
+        if (lane == 0) {
+          HPS_STAT(ST_PENDING, 1);
+          const unsigned int at = atomicAdd(pend.count, 1u);
+          if (at < pend.cap) pend.list[at] = p;
+        }
+      } else {
+        unsigned int at = 0;
+        if (lane == 0) at = atomicAdd(cont.count, 1u);
+        at = __shfl_sync(0xffffffffu, at, 0);
+        PlanState<MAXS>& ps = states[at];
+        for (int s = lane; s < r.S; s += 32) {
+          ps.ent[s] = w.ent[s];
+          ps.kmin[s] = (int32_t)w.kmin[s];
+          ps.kmax[s] = (int32_t)w.kmax[s];
+        }
+        for (int s = lane; s <= r.S; s += 32) ps.pre[s] = w.pre[s];
+        if (lane == 0) {
+          ps.p = p;
+          ps.rank_hi = (uint64_t)(rank >> 64);
+          ps.rank_lo = (uint64_t)rank;
+          ps.tau_lo = tau_lo;
+          ps.tau_hi = tau_hi;
+          ps.S = r.S;
+          ps.n_cand = n_cand;
+        }
+      }
+    } else if (!ARGMIN) {
+      write_plan<MAXS>(c, w, o, p, r);
+    } else {
+      const int code = r.status & 0x7f;
+      if (code == HPS_ST_NO_CPU_TYPE) flags |= 1u;
+      if (code == HPS_ST_INVALID) flags |= 2u;
+      const bool take = feasible_only ? false : (code != HPS_ST_NO_CPU_TYPE && code != HPS_ST_INVALID);
+      if (take) {
+        Key k{r.cost, (uint64_t)(rank >> 64), (uint64_t)rank, (uint32_t)r.status};
+        if (key_less(k, best)) best = k;
+      }
+    }
+    __syncwarp();
+  }
+  if (ARGMIN && lane == 0) merge_part(parts, gw, first, best, 0ull, flags);
+}
+
+#ifndef HPS_CAND_MINB
+#define HPS_CAND_MINB 32
+#endif
+template <int MAXS, int WARPS, bool ARGMIN>
+__global__ void __launch_bounds__(WARPS * 32, HPS_CAND_MINB / WARPS)
+candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Outputs o,
+                 int feasible_only, KeyPart* parts, int first) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
+  SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmem<MAXS>) * WARPS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem<MAXS>& w = sm[warp];
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
+  const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
+  const unsigned int n = *cont.count;
+  Key best;
+  best.cost = __longlong_as_double(0x7ff0000000000000LL);
+  best.hi = best.lo = ~0ull;
+  best.status = 0;
+  unsigned long long feas = 0;
+  uint32_t flags = 0;
+  for (uint64_t q = gw; q < n; q += nw) {
+    const PlanState<MAXS>& ps = states[q];
+    const int S = ps.S;
+    for (int s = lane; s < S; s += 32) {
+      const int e = ps.ent[s];
+      const StageEntry st = tb.stages[e];
+      w.st[s] = st;
+      w.ent[s] = e;
+      w.row[s] = tb.te + c.te_off[st.type] + (int64_t)(e - st.type * c.P) * (int64_t)(c.et_cap[st.type] + 1);
+      w.kmin[s] = (double)ps.kmin[s];
+      w.kmax[s] = (double)ps.kmax[s];
+    }
+    for (int s = lane; s <= S; s += 32) w.pre[s] = ps.pre[s];
+    __syncwarp();
+    PlanOut r;
+    r.ps = 0;
+    r.gap = 0.0;
+    r.S = S;
+    const double tau = phase_candidates_fast<MAXS>(c, tb, w, ss[warp], S, ps.tau_lo, ps.tau_hi, ps.n_cand);
+    if (tau != tau) {
+      r.status = HPS_ST_NO_CANDIDATE;
+      r.gap = 1.0;
+      r.cost = c.penalty_scale * (1.0 + 1.0);
+    } else {
+      phase_final<MAXS, true>(c, tb, w, S, tau, r);
+    }
+    if (!ARGMIN) {
+      write_plan<MAXS>(c, w, o, ps.p, r);
+    } else {
+      const int code = r.status & 0x7f;
+      if (code == HPS_ST_OK) feas++;
+      if (code == HPS_ST_NO_CPU_TYPE) flags |= 1u;
+      const bool take = feasible_only ? (code == HPS_ST_OK) : (code != HPS_ST_NO_CPU_TYPE && code != HPS_ST_INVALID);
+      if (take) {
+        Key k{r.cost, ps.rank_hi, ps.rank_lo, (uint32_t)r.status};
+        if (key_less(k, best)) best = k;
+      }
+    }
+    __syncwarp();
+  }
+  if (ARGMIN && lane == 0) merge_part(parts, gw, first, best, feas, flags);
+}
+
 template <int MAXS, int WARPS, bool ARGMIN, bool FAST, int SRC>
 int launch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
                 int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
@@ -735,17 +905,61 @@ int launch_src(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs
 template <bool ARGMIN>
 int dispatch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
                   int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
-  if (in->fast) {
-    if (in->c.L <= 16) return launch_src<16, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
-    if (in->c.L <= 32) return launch_src<32, 4, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
-    return launch_src<64, 2, ARGMIN, true>(in, src, n, o, pend, feasible_only, parts, grid, st);
-  }
   if (in->c.L <= 16) return launch_src<16, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
   if (in->c.L <= 32) return launch_src<32, 4, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
   return launch_src<64, 2, ARGMIN, false>(in, src, n, o, pend, feasible_only, parts, grid, st);
 }
 
 int warps_per_block(const HpsInstance* in) { return (in->c.L <= 32) ? 4 : 2; }
+
+template <int MAXS, int WARPS, bool ARGMIN, int SRC>
+int launch_stage(HpsInstance* in, const PlanSource& src, uint64_t p0, uint64_t p1, const Outputs& o,
+                 Pending pend, Cont cont, int feasible_only, KeyPart* parts, int first, int grid,
+                 cudaStream_t st) {
+  const size_t smem = sizeof(WarpSmem<MAXS>) * WARPS;
+  auto kern = stage_kernel<MAXS, WARPS, ARGMIN, SRC>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, WARPS * 32, smem, st>>>(in->c, in->tb, src, p0, p1, o, pend, cont, feasible_only, parts, first);
+  CUDA_TRY(cudaGetLastError());
+  return HPS_OK;
+}
+
+// chunked K1a/K1b pair over plans [0, n); parts holds 2 * grid * WARPS partial keys
+template <int MAXS, int WARPS, bool ARGMIN>
+int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
+              int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
+  const uint64_t chunk = std::min<uint64_t>(n, MAXS <= 16 ? (4ull << 20) : (MAXS <= 32 ? (2ull << 20) : (1ull << 20)));
+  char* buf = nullptr;
+  CUDA_TRY(cudaMallocAsync(&buf, sizeof(PlanState<MAXS>) * chunk + 256, st));
+  Cont cont{buf + 256, reinterpret_cast<unsigned int*>(buf)};
+  KeyPart* parts_a = parts;
+  KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
+  const size_t smem2 = (sizeof(WarpSmem<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
+  auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
+  CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
+    const uint64_t c1 = std::min(n, c0 + chunk);
+    const int first = (c0 == 0);
+    CUDA_TRY(cudaMemsetAsync(cont.count, 0, sizeof(unsigned int), st));
+    int rc;
+    if (src.mode == 0) rc = launch_stage<MAXS, WARPS, ARGMIN, 0>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
+    else if (src.mode == 1) rc = launch_stage<MAXS, WARPS, ARGMIN, 1>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
+    else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
+    if (rc) return rc;
+    k2<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, o, feasible_only, parts_b, first);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaFreeAsync(buf, st));
+  return HPS_OK;
+}
+
+template <bool ARGMIN>
+int dispatch_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
+                   int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
+  if (in->c.L <= 16) return run_split<16, 4, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (in->c.L <= 32) return run_split<32, 4, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  return run_split<64, 2, ARGMIN>(in, src, n, o, pend, feasible_only, parts, grid, st);
+}
 
 int grid_for(HpsInstance* in, uint64_t n_plans) {
   const int warps = warps_per_block(in);
@@ -805,7 +1019,7 @@ struct ArgminScratch {
 int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_only, HpsArgmin* d_best,
                   cudaStream_t st) {
   const int grid = grid_for(in, n);
-  const int nparts = grid * warps_per_block(in);
+  const int nparts = grid * warps_per_block(in) * (in->fast ? 2 : 1);
   const unsigned cap = (unsigned)std::min<uint64_t>(kSlowCap, std::max<uint64_t>(n, 1));
   char* buf = nullptr;
   const size_t bytes = sizeof(KeyPart) * (nparts + cap) + sizeof(unsigned long long) * cap + 64;
@@ -817,7 +1031,8 @@ int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_onl
   CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
   Pending pend{list, count, cap};
   Outputs o{};
-  int rc = dispatch_eval<true>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  int rc = in->fast ? dispatch_split<true>(in, src, n, o, pend, feasible_only, parts, grid, st)
+                    : dispatch_eval<true>(in, src, n, o, pend, feasible_only, parts, grid, st);
   if (rc) return rc;
   rc = run_slow(in, src, o, pend, 1, feasible_only, slow_parts, st);
   if (rc) return rc;
@@ -982,7 +1197,8 @@ int hps_score_plans(HpsInstance* in, const uint8_t* d_plans, int64_t n, const Hp
   unsigned int* count = reinterpret_cast<unsigned int*>(list + cap);
   CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
   Pending pend{list, count, cap};
-  int rc = dispatch_eval<false>(in, src, (uint64_t)n, o, pend, 0, nullptr, grid_for(in, n), st);
+  int rc = in->fast ? dispatch_split<false>(in, src, (uint64_t)n, o, pend, 0, nullptr, grid_for(in, n), st)
+                    : dispatch_eval<false>(in, src, (uint64_t)n, o, pend, 0, nullptr, grid_for(in, n), st);
   if (rc) return rc;
   rc = run_slow(in, src, o, pend, 0, 0, nullptr, st);
   if (rc) return rc;
