@@ -51,7 +51,7 @@ struct __align__(16) StageEntry {
   // single-precision constants for the count ESTIMATE that seeds the exact table search
   float f_rbo, f_rbd;    // B_o / oct, B_o / odt (0 when the work is 0)
   float f_oma, f_omb, f_alpha, f_beta;
-  int32_t pad0, pad1;
+  float f_coct, f_codt;  // oct / B_o, odt / B_o
   double rwo, rwd;       // fl(1/oct), fl(1/odt) (0 when the work is 0): certified counts
 };
 
@@ -79,6 +79,12 @@ __device__ __forceinline__ double rcp_1nt(double x) {
 }
 
 __device__ __forceinline__ double dmax_nn(double a, double b) { return a > b ? a : b; }  // no NaNs
+
+__device__ __forceinline__ float rcp_approx_f32(float x) {  // MUFU.RCP, rel. error ~2^-23
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 static __device__ HPS_NOINLINE_RARE int count_cert(const StageEntry& s, double tau, double bo) {
   const double A = tau * bo;  // identical to the reference's first product
@@ -109,6 +115,33 @@ static __device__ HPS_NOINLINE_RARE int count_cert(const StageEntry& s, double t
   HPS_STAT(ST_CERT, 1);
   if (c_lo != c_hi || !(c_hi < 2.0e9)) { HPS_STAT(ST_CERT_FAIL, 1); return -1; }
   return c_lo < 1.0 ? 1 : (int)c_lo;
+}
+
+// One-sided count bounds in FP32 for pruning only: returns lower bound kl <= count(tau) and
+// upper bound ku >= count(tau) (ku = 0 when no bound could be established). Relative error of
+// every FP32 quantity is bounded by a few 2^-24; with kappa = B/h the headroom's relative
+// error is <= 3e-7 (kappa + 1), so q in q~ (1 +- 4e-7 (kappa + 2)). floor(q_lo) <= ceil(q - 1e-9).
+__device__ __forceinline__ void count_bounds32(const StageEntry& s, float tau, int& kl, int& ku) {
+  float lo = 1.0f, hi = 1.0f;
+  bool ok = true;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const float rb = side ? s.f_rbd : s.f_rbo;
+    if (rb == 0.0f) continue;  // work == 0
+    const float frac = side ? s.f_beta : s.f_alpha;
+    const float omf = side ? s.f_omb : s.f_oma;
+    const float B = tau * rb;
+    const float h = B - omf;
+    if (frac == 0.0f) continue;  // contributes nothing (in range no raise)
+    if (!(h > 1e-3f * B)) { ok = false; continue; }  // too much cancellation: no upper bound
+    const float rh = rcp_approx_f32(h);
+    const float q = frac * rh;
+    const float e = 4e-7f * (B * rh + 2.0f) + 1e-6f;
+    lo = fmaxf(lo, q * (1.0f - e));
+    hi = fmaxf(hi, q * (1.0f + e));
+  }
+  kl = (int)floorf(lo);
+  ku = ok ? (int)ceilf(hi) + 1 : 0;
 }
 
 // et(k) approximately (k >= 1 integer): within ~4 ulp of _stage_et(s, k)

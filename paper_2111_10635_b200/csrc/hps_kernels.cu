@@ -629,7 +629,8 @@ __global__ void stage_table_kernel(const InstanceConsts c, RawTables raw, StageE
   e.f_omb = (float)e.omb;
   e.f_alpha = (float)e.alpha;
   e.f_beta = (float)e.beta;
-  e.pad0 = e.pad1 = 0;
+  e.f_coct = (float)e.c_oct;
+  e.f_codt = (float)e.c_odt;
   e.rwo = (e.oct != 0) ? 1.0 / e.oct : 0.0;
   e.rwd = (e.odt != 0) ? 1.0 / e.odt : 0.0;
   out[idx] = e;

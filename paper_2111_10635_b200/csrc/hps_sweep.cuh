@@ -70,21 +70,31 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<M
   return cs.work / thr * P;
 }
 
-// rigorous lower bound: exact counts of the two top stages, count(tau_hi) for the others
+// rigorous lower bound from FP32 one-sided count bounds of the two top stages and count(tau_hi)
+// for the others: P >= sum price k_lo, E >= max(pinned et, et(k_hi) of the top stages).
+// Everything FP32 carries a 1e-5 relative slack, so the bound never exceeds the exact cost.
 template <int MAXS>
 __device__ __forceinline__ double cost_bound(const CostScalars cs, const WarpSmem<MAXS>& w,
                                              const SweepSmem<MAXS>& sw, double tau) {
-  double P = sw.pmin_rest, E = sw.ep_max;
+  const float tf = (float)tau;
+  float P = (float)sw.pmin_rest, E = (float)sw.ep_max;
 #pragma unroll
   for (int q = 0; q < 2; q++) {
     const int r = sw.top[q];
     if (r < 0) continue;
-    const int k = count_fast<MAXS>(cs.bo, w, r, tau);
-    P += sw.pr[r] * (double)k;
-    E = fmax(E, w.row[r][k - 1].et);
+    int kl, ku;
+    count_bounds32(w.st[r], tf, kl, ku);
+    const int lo = (int)w.kmin[r], hi = (int)w.kmax[r];
+    kl = max(kl, lo);
+    P += (float)sw.pr[r] * (float)kl;
+    if (ku > 0) {
+      const StageEntry& st = w.st[r];
+      const float k = (float)min(ku, hi);
+      const float rk = rcp_approx_f32(k);
+      E = fmaxf(E, fmaxf(st.f_coct * (st.f_oma + st.f_alpha * rk), st.f_codt * (st.f_omb + st.f_beta * rk)));
+    }
   }
-  // cost_ref = fl(fl(work / fl(batch / E)) * P_seq) >= (work / batch) E P (1 - 1e-13)
-  return cs.work / cs.batch * E * P * (1.0 - 1e-13);
+  return (double)((float)(cs.work / cs.batch) * E * P) * (1.0 - 1e-5);
 }
 
 template <int MAXS>
@@ -138,22 +148,22 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   buf.init();
   const int rounds = (n_cand + 31) >> 5;
   int sp = 0;
-  for (int jr = 0; jr < rounds; jr += 8) {  // warm start: every 8th round exactly
-    const int i = jr * 32 + lane;
-    if (i >= n_cand) break;
+  {  // warm start: one round of 32 candidates spread evenly over the candidate range
+    const int i = (int)(((long long)lane * n_cand) >> 5);
     const double tau = cand_tau<MAXS>(w, i, sp, tau_lo, tau_hi);
-    if (!(tau >= tau_lo && tau <= tau_hi)) continue;
-    HPS_STAT(ST_CANDS, 1);
-    buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau), tau);
+    if (tau >= tau_lo && tau <= tau_hi) {
+      HPS_STAT(ST_CANDS, 1);
+      buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau), tau);
+    }
   }
   double ub = warp_min(buf.mn);
-  // the other rounds: lower-bound filter; survivors are compacted into sw.q and evaluated
-  // densely (a warp only saves work when all 32 lanes skip, so skipping must be compacted)
+  // every candidate: lower-bound filter; survivors are compacted into sw.q and evaluated
+  // densely (a warp only saves work when all 32 lanes skip, so skipping must be compacted).
+  // A warm-start candidate may pass again; re-inserting it is harmless (same cost and tau).
   sp = 0;
   int qn = 0;
   const unsigned lt = (1u << lane) - 1u;
   for (int jr = 0; jr < rounds; jr++) {
-    if ((jr & 7) == 0) continue;
     const int i = jr * 32 + lane;
     bool keep = false;
     double tau = 0.0;
