@@ -179,7 +179,56 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
   }
   present = __reduce_or_sync(0xffffffffu, (ty[0] >= 0 ? 1u << ty[0] : 0u) | (ty[1] >= 0 ? 1u << ty[1] : 0u));
   int it = 0;
+  {  // probes below L* = max_r theta_r(Q): some stage is over its quota, so quota_ok fails
+    double lstar = -__longlong_as_double(0x7ff0000000000000LL);
+    for (int slot = 0; slot < 2; slot++)
+      if (ty[slot] >= 0) lstar = fmax(lstar, thq[slot]);
+    lstar = warp_max(lstar);
+    for (; it < 60; it++) {
+      const double mid = (a + b) / 2.0;
+      if (!(mid < lstar)) break;
+      a = mid;
+    }
+  }
+  bool closed = false;
+  double tstar_single = 0.0;
   for (; it < 60; it++) {
+    // (1) each type has at most one unresolved stage r: on (a, b) its type's constraint is
+    //     count_r(mid) <= K_r = Q_t - sum of the type's other (pinned) counts, i.e.
+    //     mid >= theta_r(K_r); quota_ok switches at the max of those thresholds.
+    {
+      const bool u0 = ty[0] >= 0 && ub[0] != lb[0], u1 = ty[1] >= 0 && ub[1] != lb[1];
+      const unsigned tm = (u0 ? 1u << ty[0] : 0u) | (u1 ? 1u << ty[1] : 0u);
+      const unsigned types_u = __reduce_or_sync(0xffffffffu, tm);
+      bool single = !(u0 && u1 && ty[0] == ty[1]);
+      single = __all_sync(0xffffffffu, single);
+      unsigned rem = types_u;
+      while (single && rem) {
+        const int t = __ffs(rem) - 1;
+        rem &= rem - 1;
+        single = __popc(__ballot_sync(0xffffffffu, (tm >> t) & 1u)) <= 1;
+      }
+      if (single && types_u) {
+        double th = -__longlong_as_double(0x7ff0000000000000LL);
+        unsigned rem2 = types_u;
+        while (rem2) {
+          const int t = __ffs(rem2) - 1;
+          rem2 &= rem2 - 1;
+          const unsigned v = (ty[0] == t ? (unsigned)lb[0] : 0u) + (ty[1] == t ? (unsigned)lb[1] : 0u);
+          const long long sum_b = (long long)__reduce_add_sync(0xffffffffu, v);  // counts at b
+          for (int slot = 0; slot < 2; slot++) {
+            const bool mine = (slot ? u1 : u0) && ty[slot] == t;
+            if (mine) {
+              const long long K = c.quota[t] - (sum_b - lb[slot]);  // >= lb (quota_ok(b))
+              th = fmax(th, row[slot][(int)K].th);                  // count <= K <=> tau >= theta(K)
+            }
+          }
+        }
+        tstar_single = warp_max(th);
+        closed = true;
+        break;
+      }
+    }
     const bool wide = (ub[0] - lb[0] > 1 && ub[0] != kOver) || (ub[1] - lb[1] > 1 && ub[1] != kOver) ||
                       (ub[0] == kOver && lb[0] < Q[0]) || (ub[1] == kOver && lb[1] < Q[1]);
     if (!__any_sync(0xffffffffu, wide)) break;
@@ -210,11 +259,27 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
       }
     }
     const bool any_over = __any_sync(0xffffffffu, over);
-    const bool ok = !any_over && quota_sums_ok(c, present, ty[0], km[0], ty[1], km[1]);
+    // counts at b satisfy the quotas; only a count above its value at b can break them
+    const bool rose = __any_sync(0xffffffffu, km[0] != lb[0] || km[1] != lb[1]);
+    const bool ok = !any_over && (!rose || quota_sums_ok(c, present, ty[0], km[0], ty[1], km[1]));
     if (ok) { b = mid; lb[0] = km[0]; lb[1] = km[1]; }
     else { a = mid; ub[0] = km[0]; ub[1] = km[1]; }
   }
-  if (it < 60) {
+  if (closed) {
+    if (lane == 0) HPS_STAT(ST_PROBES_CLOSED, 60 - it);
+    for (; it < 60; it++) {
+      const double mid = (a + b) / 2.0;
+      if (mid >= tstar_single) b = mid; else a = mid;
+    }
+    // counts at the final b: unresolved stages resolve by their threshold
+    for (int slot = 0; slot < 2; slot++)
+      if (ty[slot] >= 0 && ub[slot] != lb[slot]) {
+        const int hi = (ub[slot] == kOver) ? Q[slot] : ub[slot];
+        const int kc = count_cert(st[lane + 32 * slot], b, c.bo);
+        lb[slot] = (kc >= lb[slot] && kc <= hi) ? kc
+                                                 : count_tab(row[slot], b, lb[slot], hi, est_count(st[lane + 32 * slot], b));
+      }
+  } else if (it < 60) {
     // every unpinned stage has count(a) == count(b) + 1 (or "over" with count(b) == Q):
     // on (a, b) its count is lb + [tau < theta(lb)], so quota_ok switches at one of those
     // thresholds (or stays true up to b). Find the switch point tau* exactly.
