@@ -19,6 +19,8 @@
  *   hps_random_argmin     random_search non-dedup path (ls/baselines.py:230-282): the plans
  *                         are numpy default_rng(seed).integers(0,T,L), generated in-kernel
  *   hps_report            evaluate (ls/costmodel.py:102-167) per-stage times for given counts
+ *   hps_score_plans_static  PlanScorer(mode='staratio'|'stapsratio') -> static_provision ->
+ *                         evaluate (ls/provisioner.py:516-561, ls/scoring.py:79-101)
  *   hps_pcg64_*           numpy PCG64 / Generator.integers / Generator.random replicas used
  *                         by the searchers and the policy sampler (ls/policy/network.py:251-262)
  */
@@ -60,6 +62,8 @@ enum {
   HPS_ST_NO_CPU_TYPE = 8,    /* accelerator units but no CPU type: the reference raises
                                 InvariantError (not data); the shim re-raises it            */
   HPS_ST_INVALID = 9,        /* plan id out of range: PlanValidationError                    */
+  HPS_ST_STATIC_NONE = 10,   /* static mode: no ratio multiple within quota meets the limit
+                                (InfeasibleError gap=1.0)          ls/provisioner.py:557-561 */
   HPS_ST_OVERFLOW_FLAG = 0x80 /* OR-ed in when the >4096-breakpoint path ran (:456-470)       */
 };
 
@@ -164,6 +168,17 @@ int hps_report(HpsInstance* inst, const uint8_t* d_plans, const int32_t* d_k,
                const int32_t* d_ps, int64_t n, double* d_ct, double* d_dt, double* d_et,
                double* d_tp, double* d_pipeline_tp, double* d_exec_time, double* d_cost,
                uint8_t* d_feasible, void* stream);
+
+/* Static provisioning baselines (ls/provisioner.py:516-561): the smallest multiplier g with
+ * 1 accelerator unit per accelerator stage and `cpu_per_gpu` cores per CPU stage that meets
+ * the throughput limit within quota; mode HPS_MODE_STAPSRATIO also charges cpu_per_gpu
+ * parameter-server cores per accelerator unit on the cheapest CPU type. Same outputs as
+ * hps_score_plans; the instance's ProvisionerConfig and with_ps are not used (as in the
+ * reference). A catalog without a CPU type gives HPS_ST_NO_CPU_TYPE for every valid plan
+ * (ls/provisioner.py:538 raises before the scan). */
+enum { HPS_MODE_STARATIO = 1, HPS_MODE_STAPSRATIO = 2 };
+int hps_score_plans_static(HpsInstance* inst, const uint8_t* d_plans, int64_t n, int32_t mode,
+                           int32_t cpu_per_gpu, const HpsPlanResults* results, void* stream);
 
 /* ---- scheduling policy on the device (K3-K6) -----------------------------------------------
  * Replaces policy_forward / sample_actions / the train() round body / policy_gradient /

@@ -21,12 +21,15 @@ LIB_PATH = PKG_DIR / "libhps.so"
 # per-plan status byte (include/hps.h HPS_ST_*)
 ST_OK, ST_MIN_K1, ST_SERIAL, ST_QUOTA_TAU_HI, ST_FLOOR_TAU_HI = 0, 1, 2, 3, 4
 ST_NO_CANDIDATE, ST_PS_QUOTA, ST_DEFENSIVE, ST_NO_CPU_TYPE, ST_INVALID = 5, 6, 7, 8, 9
+ST_STATIC_NONE = 10
 ST_OVERFLOW_FLAG = 0x80
 ST_CODE_MASK = 0x7F
 STATUS_NAMES = {ST_OK: "ok", ST_MIN_K1: "min_k1", ST_SERIAL: "serial",
                 ST_QUOTA_TAU_HI: "quota_at_tau_hi", ST_FLOOR_TAU_HI: "floor_at_tau_hi",
                 ST_NO_CANDIDATE: "no_candidate", ST_PS_QUOTA: "ps_quota",
-                ST_DEFENSIVE: "defensive", ST_NO_CPU_TYPE: "no_cpu_type", ST_INVALID: "invalid"}
+                ST_DEFENSIVE: "defensive", ST_NO_CPU_TYPE: "no_cpu_type", ST_INVALID: "invalid",
+                ST_STATIC_NONE: "static_none"}
+MODE_CODES = {"staratio": 1, "stapsratio": 2}   # HPS_MODE_* (include/hps.h)
 
 HPS_OK, HPS_E_INVALID_ARG, HPS_E_PLAN, HPS_E_CONFIG, HPS_E_CUDA = 0, 1, 2, 3, 4
 HPS_E_NO_CPU_TYPE, HPS_E_NUMERIC = 5, 6
@@ -151,6 +154,8 @@ _SIGNATURES = {
     "hps_policy_last_error": (C.c_char_p, []),
     "hps_probe_fp64": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "hps_stats_read": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "hps_score_plans_static": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                         C.c_void_p, C.c_void_p]),
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),
 }
 

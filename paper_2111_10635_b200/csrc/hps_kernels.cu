@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1349,6 +1350,145 @@ extern "C" int hps_report(HpsInstance* in, const uint8_t* d_plans, const int32_t
   if (n == 0) return HPS_OK;
   report_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       in->c, in->tb, d_plans, d_k, d_ps, n, d_ct, d_dt, d_et, d_tp, d_pipeline_tp, d_exec_time, d_cost, d_feasible);
+  CUDA_TRY(cudaGetLastError());
+  return HPS_OK;
+}
+
+// ---- static provisioning baselines (ls/provisioner.py:516-561) --------------------------------
+namespace {
+// One thread per plan. Counts are linear in the multiplier g (k_s = f_s * g, per-type totals
+// m_t * g), so the quota break of the reference's scan is g_max = min_t floor(Q_t / m_t); the
+// throughput test is monotone in g whenever every stage's ct/dt coefficients are >= 0 (et is
+// then non-increasing in k under IEEE rounding), so the first feasible g is found by bisection
+// over [1, g_max]. Otherwise the scan runs literally.
+__device__ bool static_feasible(const InstanceConsts& c, const StageEntry* const* ent, const int* f,
+                                int S, long long g, double& overall) {
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  overall = inf;
+  for (int s = 0; s < S; s++) {
+    const double kk = (double)((long long)f[s] * g);
+    const double x = stage_et(*ent[s], kk);
+    const double tp = (x > 0) ? c.batch / x : inf;
+    overall = (s == 0) ? tp : pmin(overall, tp);
+  }
+  return overall > c.limit;
+}
+
+__global__ void static_kernel(const InstanceConsts c, const DeviceTables tb, const uint8_t* plans, int64_t n,
+                              int mode, int cpu_per_gpu, Outputs o) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int L = c.L;
+  const uint8_t* pl = plans + i * L;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  int32_t* kout = o.k ? o.k + i * L : nullptr;
+  if (kout) for (int s = 0; s < L; s++) kout[s] = 0;
+  for (int l = 0; l < L; l++) {
+    if (pl[l] >= c.T) {   // validate_plan (ls/provisioner.py:536)
+      o.cost[i] = nan; o.status[i] = HPS_ST_INVALID;
+      if (o.gap) o.gap[i] = 0.0;
+      if (o.ps) o.ps[i] = 0;
+      if (o.num_stages) o.num_stages[i] = 0;
+      return;
+    }
+  }
+  const StageEntry* ent[kMaxL];
+  int f[kMaxL];
+  int order[kMaxT + 1];
+  long long m[kMaxT + 1];
+  int nt = 0, S = 0, start = 0;
+  long long n_acc = 0;
+  bool mono = c.batch >= 0.0;
+  for (int pos = 1; pos <= L; pos++) {   // build_stages (ls/domain.py:293-296)
+    if (pos < L && pl[pos] == pl[start]) continue;
+    const int t = pl[start];
+    ent[S] = &tb.stages[entry_index(c.P, t, start, pos - 1)];
+    f[S] = c.is_cpu[t] ? cpu_per_gpu : 1;
+    if (!c.is_cpu[t]) n_acc++;
+    mono = mono && ent[S]->c_oct >= 0.0 && ent[S]->alpha >= 0.0 && ent[S]->c_odt >= 0.0 &&
+           ent[S]->beta >= 0.0;
+    int j = 0;
+    while (j < nt && order[j] != t) j++;
+    if (j == nt) { order[nt] = t; m[nt] = 0; nt++; }
+    m[j] += f[S];
+    S++;
+    start = pos;
+  }
+  if (o.num_stages) o.num_stages[i] = S;
+  if (c.ps_type < 0) {   // catalog.cheapest_cpu_type() raises first (ls/provisioner.py:538)
+    o.cost[i] = nan; o.status[i] = HPS_ST_NO_CPU_TYPE;
+    if (o.gap) o.gap[i] = 0.0;
+    if (o.ps) o.ps[i] = 0;
+    return;
+  }
+  const long long ps_per_g = (mode == 2) ? (long long)cpu_per_gpu * n_acc : 0;
+  if (ps_per_g > 0) {
+    int j = 0;
+    while (j < nt && order[j] != c.ps_type) j++;
+    if (j == nt) { order[nt] = c.ps_type; m[nt] = 0; nt++; }
+    m[j] += ps_per_g;
+  }
+  // over_quota(g) <=> some m_t * g > Q_t; max_quota bounds the scan (ls/provisioner.py:539-552)
+  long long gmax = LLONG_MAX;
+  long long maxq = 0;
+  for (int t = 0; t < c.T; t++) maxq = (c.quota[t] > maxq) ? c.quota[t] : maxq;
+  for (int j = 0; j < nt; j++) {
+    if (m[j] <= 0) continue;
+    const long long q = c.quota[order[j]];
+    const long long gm = (q < 0) ? -1 : q / m[j];
+    gmax = (gm < gmax) ? gm : gmax;
+  }
+  gmax = (maxq < gmax) ? maxq : gmax;
+  long long g_found = 0;
+  double overall = 0.0;
+  if (gmax >= 1) {
+    if (mono) {
+      if (static_feasible(c, ent, f, S, gmax, overall)) {
+        long long lo = 0, hi = gmax;   // feasible(hi), !feasible(lo) (lo = 0 is a sentinel)
+        while (hi - lo > 1) {
+          const long long mid = lo + (hi - lo) / 2;
+          double ov;
+          if (static_feasible(c, ent, f, S, mid, ov)) hi = mid; else lo = mid;
+        }
+        g_found = hi;
+      }
+    } else {
+      for (long long g = 1; g <= gmax; g++) {
+        double ov;
+        if (static_feasible(c, ent, f, S, g, ov)) { g_found = g; break; }
+      }
+    }
+  }
+  if (g_found == 0) {   // InfeasibleError(gap=1.0) -> penalty_cost (ls/provisioner.py:557-561)
+    o.cost[i] = c.penalty_scale * (1.0 + 1.0); o.status[i] = HPS_ST_STATIC_NONE;
+    if (o.gap) o.gap[i] = 1.0;
+    if (o.ps) o.ps[i] = 0;
+    return;
+  }
+  static_feasible(c, ent, f, S, g_found, overall);
+  // evaluate(): exec time and cost over per_type_totals in insertion order (ls/costmodel.py:90-99)
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const double ex = (overall > 0 && overall != inf) ? c.work / overall : 0.0;
+  double per_second = 0.0;
+  for (int j = 0; j < nt; j++) per_second += c.price_h[order[j]] / 3600.0 * (double)(m[j] * g_found);
+  o.cost[i] = ex * per_second;
+  o.status[i] = HPS_ST_OK;
+  if (o.gap) o.gap[i] = 0.0;
+  if (o.ps) o.ps[i] = (int32_t)(ps_per_g * g_found);
+  if (kout) for (int s = 0; s < S; s++) kout[s] = (int32_t)((long long)f[s] * g_found);
+}
+}  // namespace
+
+extern "C" int hps_score_plans_static(HpsInstance* in, const uint8_t* d_plans, int64_t n, int32_t mode,
+                                      int32_t cpu_per_gpu, const HpsPlanResults* r, void* stream) {
+  if (!in || !r || !r->cost || !r->status || n < 0) return set_err(HPS_E_INVALID_ARG, "null argument");
+  if (mode != HPS_MODE_STARATIO && mode != HPS_MODE_STAPSRATIO)
+    return set_err(HPS_E_INVALID_ARG, "unknown static provisioning mode");
+  if (cpu_per_gpu < 1) return set_err(HPS_E_INVALID_ARG, "cpu_per_gpu must be >= 1");
+  if (n == 0) return HPS_OK;
+  Outputs o{r->cost, r->status, r->gap, r->ps, r->num_stages, r->k};
+  static_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(in->c, in->tb, d_plans, n, mode,
+                                                                               cpu_per_gpu, o);
   CUDA_TRY(cudaGetLastError());
   return HPS_OK;
 }

@@ -79,8 +79,12 @@ class DeviceInstance:
         return tuple(out)
 
     # ---- K1: batched PlanScorer ----
-    def score(self, plans, want_k: bool = True, stream=None) -> dict:
-        """Score plans (uint8 [n, L] tensor on this device). Returns device tensors."""
+    def score(self, plans, want_k: bool = True, stream=None, mode: str = "optimal",
+              cpu_per_gpu: int = 6) -> dict:
+        """Score plans (uint8 [n, L] tensor on this device). Returns device tensors.
+
+        ``mode`` 'staratio' / 'stapsratio' runs the static provisioning baselines
+        (ls/provisioner.py:516-561) instead of optimize_k1 + add_ps_cores."""
         if plans.dtype != torch.uint8 or plans.dim() != 2 or plans.shape[1] != self.L:
             raise ConfigError(f"plans must be uint8 [n, {self.L}]")
         plans = plans.to(self.device).contiguous()
@@ -95,8 +99,15 @@ class DeviceInstance:
         res = _abi.HpsPlanResults(*(out[k].data_ptr() if out[k] is not None else None
                                     for k in ("cost", "status", "gap", "ps", "num_stages", "k")))
         with torch.cuda.device(dev):
-            _abi.check(self.lib.hps_score_plans(self.handle, _ptr(plans), n, C.byref(res),
-                                                _stream(stream)), "hps_score_plans")
+            if mode == "optimal":
+                _abi.check(self.lib.hps_score_plans(self.handle, _ptr(plans), n, C.byref(res),
+                                                    _stream(stream)), "hps_score_plans")
+            else:
+                if mode not in _abi.MODE_CODES:
+                    raise ConfigError(f"unknown provisioning mode '{mode}'")
+                _abi.check(self.lib.hps_score_plans_static(
+                    self.handle, _ptr(plans), n, _abi.MODE_CODES[mode], int(cpu_per_gpu),
+                    C.byref(res), _stream(stream)), "hps_score_plans_static")
         return out
 
     # ---- K2: fused enumeration / random sweep argmin ----

@@ -25,6 +25,7 @@ MODE_OPTIMAL = "optimal"      # ls/provisioner.py:51-54
 MODE_STARATIO = "staratio"
 MODE_STAPSRATIO = "stapsratio"
 PROVISIONING_MODES = (MODE_OPTIMAL, MODE_STARATIO, MODE_STAPSRATIO)
+STATIC_CPU_PER_GPU = 6        # ls/provisioner.py:47
 
 
 def _check_fraction(layer: int, name: str, table: Mapping[int, float]) -> None:

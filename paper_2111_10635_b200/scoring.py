@@ -13,8 +13,8 @@ from collections import OrderedDict
 import numpy as np
 
 from . import _abi
-from .errors import ConfigError, InfeasibleError, InvariantError, PlanValidationError
-from .model import (MODE_OPTIMAL, PROVISIONING_MODES, CostReport, JobParams, ProvisionerConfig,
+from .errors import InfeasibleError, InvariantError, PlanValidationError
+from .model import (MODE_OPTIMAL, MODE_STAPSRATIO, MODE_STARATIO, PROVISIONING_MODES, STATIC_CPU_PER_GPU, CostReport, JobParams, ProvisionerConfig,
                     ProvisioningPlan, ResourceCatalog, ResourceType, ScoredPlan, SchedulingPlan,
                     Stage, penalty_cost)
 
@@ -28,6 +28,7 @@ _MESSAGES = {
     _abi.ST_FLOOR_TAU_HI: "a stage cannot reach the load-balance target at any count",
     _abi.ST_NO_CANDIDATE: "no count within quota meets the throughput limit strictly",
     _abi.ST_PS_QUOTA: "the CPU type cannot host the parameter-server cores within its quota",
+    _abi.ST_STATIC_NONE: "no ratio multiple within quota meets the throughput limit",
 }
 
 _INSTANCES: "OrderedDict[tuple, object]" = OrderedDict()
@@ -105,9 +106,6 @@ class PlanScorer:
                  mode: str = MODE_OPTIMAL, with_ps: bool = True):
         if mode not in PROVISIONING_MODES:
             raise InvariantError(f"unknown provisioning mode '{mode}'")
-        if mode != MODE_OPTIMAL:
-            raise ConfigError(f"provisioning mode '{mode}' is not implemented on the device "
-                              "(static modes are the next item of SURVEY.md §8(f))")
         self.graph, self.catalog, self.params, self.config = graph, catalog, params, config
         self.mode, self.with_ps = mode, with_ps
         self.evaluations = 0
@@ -132,7 +130,8 @@ class PlanScorer:
         import torch
         if not torch.is_tensor(plans_u8):
             plans_u8 = torch.from_numpy(np.ascontiguousarray(plans_u8, dtype=np.uint8))
-        return self.instance.score(plans_u8.to(self.instance.device), want_k=want_k)
+        return self.instance.score(plans_u8.to(self.instance.device), want_k=want_k,
+                                   mode=self.mode, cpu_per_gpu=STATIC_CPU_PER_GPU)
 
     def score_many(self, plans) -> list:
         import torch
@@ -189,14 +188,66 @@ class PlanScorer:
 
 def provision(plan, graph, catalog, params, config: ProvisionerConfig = ProvisionerConfig(),
               mode: str = MODE_OPTIMAL, with_ps: bool = True) -> ProvisioningPlan:
-    """ls/provisioner.py:564-584 on the device; raises InfeasibleError(gap) like the reference."""
+    """ls/provisioner.py:564-584 on the device; raises InfeasibleError(gap) like the reference.
+
+    ``mode`` 'staratio' / 'stapsratio' dispatches to static_provision (ls/provisioner.py:516-561).
+    """
+    if mode not in PROVISIONING_MODES:
+        raise InvariantError(f"unknown provisioning mode '{mode}'")
     validate_plan(plan, graph, catalog)
-    if mode != MODE_OPTIMAL:
-        raise ConfigError(f"provisioning mode '{mode}' is not implemented on the device")
     import torch
     inst = device_instance(graph, catalog, params, config, with_ps)
-    out = inst.score(torch.tensor([list(plan.assignment)], dtype=torch.uint8))
+    out = inst.score(torch.tensor([list(plan.assignment)], dtype=torch.uint8), mode=mode,
+                     cpu_per_gpu=STATIC_CPU_PER_GPU)
+    return _provisioning_from(out, plan, graph, catalog, params, inst, mode, STATIC_CPU_PER_GPU)
+
+
+def static_provision(plan, graph, catalog, params, mode: str,
+                     cpu_per_gpu: int = STATIC_CPU_PER_GPU) -> ProvisioningPlan:
+    """Fixed-ratio provisioning baseline (ls/provisioner.py:516-561) on the device."""
+    if mode not in (MODE_STARATIO, MODE_STAPSRATIO):
+        raise InvariantError(f"unknown static provisioning mode '{mode}'")
+    validate_plan(plan, graph, catalog)
+    import torch
+    inst = device_instance(graph, catalog, params)
+    out = inst.score(torch.tensor([list(plan.assignment)], dtype=torch.uint8), mode=mode,
+                     cpu_per_gpu=cpu_per_gpu)
+    return _provisioning_from(out, plan, graph, catalog, params, inst, mode, cpu_per_gpu)
+
+
+def _static_violation(plan, catalog, params, inst, mode, cpu_per_gpu):
+    """The reference's InfeasibleError text carries the last scanned multiplier's violation
+    (ls/provisioner.py:553-561). The scan's last g is the quota bound g_max (integer
+    bookkeeping here); its throughput comes from the device evaluate()."""
+    import torch
+    runs = _runs(plan.assignment)
+    f = [cpu_per_gpu if catalog.types[t].is_cpu else 1 for t, _, _ in runs]
+    n_acc = sum(1 for t, _, _ in runs if not catalog.types[t].is_cpu)
+    per = {}
+    for (t, _, _), x in zip(runs, f):
+        per[t] = per.get(t, 0) + x
+    ps_per = cpu_per_gpu * n_acc if mode == MODE_STAPSRATIO else 0
+    if ps_per > 0:
+        cpu = catalog.cheapest_cpu_type().id
+        per[cpu] = per.get(cpu, 0) + ps_per
+    gmax = min(max(t.quota for t in catalog.types),
+               *(catalog.types[t].quota // m for t, m in per.items()))
+    if gmax < 1:
+        return None
+    k = torch.zeros((1, len(plan.assignment)), dtype=torch.int32)
+    k[0, :len(runs)] = torch.tensor([x * gmax for x in f], dtype=torch.int32)
+    rep = inst.report(torch.tensor([list(plan.assignment)], dtype=torch.uint8), k,
+                      torch.tensor([ps_per * gmax], dtype=torch.int32))
+    overall = float(rep["pipeline_tp"][0].item())
+    return (f"pipeline throughput {overall:.6g} does not strictly exceed "
+            f"limit {params.throughput_limit:.6g}")
+
+
+def _provisioning_from(out, plan, graph, catalog, params, inst, mode, cpu_per_gpu):
     code = int(out["status"][0].item()) & _abi.ST_CODE_MASK
+    if code == _abi.ST_STATIC_NONE:
+        last = _static_violation(plan, catalog, params, inst, mode, cpu_per_gpu)
+        raise InfeasibleError(_MESSAGES[code] + (f": {last}" if last else ""), gap=1.0)
     raise_for_status(code, float(out["gap"][0].item()))
     S = int(out["num_stages"][0].item())
     k = tuple(int(x) for x in out["k"][0, :S].cpu().tolist())
@@ -266,5 +317,6 @@ def build_stages(plan, graph) -> tuple:
     return tuple(stages)
 
 
-__all__ = ["PlanScorer", "ScoredPlan", "penalty_cost", "provision", "optimize_k1", "evaluate",
+__all__ = ["PlanScorer", "ScoredPlan", "penalty_cost", "provision", "static_provision",
+           "optimize_k1", "evaluate",
            "build_stages", "validate_plan", "device_instance"]
