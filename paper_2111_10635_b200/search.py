@@ -1,4 +1,5 @@
-"""Plan searchers on the device: brute_force and random_search (ls/baselines.py:63-87,230-282).
+"""Plan searchers on the device: brute_force and random_search (ls/baselines.py:63-87,230-282),
+plus greedy / genetic / heuristic_first_layer / homogeneous (ls/baselines.py:90-228).
 
 Both keep the reference's signature, cap, tie rules and returned ScoredPlan. The sweep is one
 fused kernel per GPU (in-kernel plan decode / generation + per-plan scoring + (cost, rank)
@@ -12,6 +13,9 @@ from __future__ import annotations
 import numpy as np
 
 from . import _abi
+from dataclasses import dataclass
+from typing import Sequence
+
 from .errors import ConfigError, InfeasibleError, InvariantError, PlanValidationError
 from .instance import argmin_from_bytes, pcg_from_generator
 from .model import ProvisionerConfig, ScoredPlan, SchedulingPlan
@@ -165,5 +169,135 @@ def _reference_assignments(rng, T, L, budget, dedup):
     return [tuple(int(g) for g in rng.integers(0, T, L)) for _ in range(budget)]
 
 
-__all__ = ["brute_force", "random_search", "enumerate_argmin", "allgather_argmin", "merge_keys",
+def _better(candidate, incumbent) -> bool:
+    """Strictly cheaper, or equally cheap with a lexicographically smaller plan
+    (ls/baselines.py:54-60)."""
+    if incumbent is None:
+        return True
+    if candidate.cost != incumbent.cost:
+        return candidate.cost < incumbent.cost
+    return candidate.plan.assignment < incumbent.plan.assignment
+
+
+def greedy(graph, catalog, params, config: ProvisionerConfig = ProvisionerConfig()) -> ScoredPlan:
+    """Left-to-right layer fixing with suffix fill (ls/baselines.py:90-117). The T candidates of
+    each layer are one device batch; ties go to the lower type id."""
+    T, L = catalog.num_types, graph.num_layers
+    scorer = PlanScorer(graph, catalog, params, config)
+    decided: list = []
+    for _ in range(L):
+        cands = [tuple(decided) + (t,) * (L - len(decided)) for t in range(T)]
+        scored = scorer.score_many(cands)
+        best_type, best = 0, None
+        for t, sc in enumerate(scored):
+            if best is None or sc.cost < best.cost:
+                best, best_type = sc, t
+        decided.append(best_type)
+    final = scorer(SchedulingPlan(tuple(decided)))
+    return ScoredPlan(final.plan, final.provisioning, final.cost, final.report, scorer.evaluations)
+
+
+@dataclass(frozen=True)
+class GeneticConfig:
+    """Genetic-search knobs (ls/baselines.py:30-51); ``mutation_rate=None`` means 1/L."""
+    population: int = 64
+    generations: int = 200
+    crossover_rate: float = 0.8
+    mutation_rate: float | None = None
+    tournament_size: int = 3
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.population < 2:
+            raise InvariantError("population must be >= 2")
+        if not 0.0 <= self.crossover_rate <= 1.0:
+            raise InvariantError("crossover_rate must be in [0, 1]")
+        if self.mutation_rate is not None and not 0.0 <= self.mutation_rate <= 1.0:
+            raise InvariantError("mutation_rate must be in [0, 1]")
+        if self.tournament_size < 1:
+            raise InvariantError("tournament_size must be >= 1")
+        if self.generations < 0:
+            raise InvariantError("generations must be >= 0")
+
+
+def genetic(graph, catalog, params, config: GeneticConfig = GeneticConfig(),
+            provisioner_config: ProvisionerConfig = ProvisionerConfig(),
+            seed_plans: Sequence = ()) -> ScoredPlan:
+    """Tournament selection, one-point crossover, per-gene mutation, one elite
+    (ls/baselines.py:120-187). The RNG draws are the reference's numpy Generator calls in the
+    same order; each generation's population is scored as one device batch."""
+    T, L = catalog.num_types, graph.num_layers
+    mutation_rate = config.mutation_rate if config.mutation_rate is not None else 1.0 / L
+    rng = np.random.default_rng(config.seed)
+    scorer = PlanScorer(graph, catalog, params, provisioner_config)
+    population = [p.assignment for p in seed_plans][:config.population]
+    while len(population) < config.population:
+        population.append(tuple(int(g) for g in rng.integers(0, T, L)))
+    best = None
+
+    def evaluate_population(pop):
+        nonlocal best
+        scored = scorer.score_many(pop)
+        for sc in scored:
+            if _better(sc, best):
+                best = sc
+        return scored
+
+    scored = evaluate_population(population)
+    for _ in range(config.generations):
+        costs = np.array([sc.cost for sc in scored])
+        children = [population[int(np.argmin(costs))]]
+        while len(children) < config.population:
+            parents = []
+            for _ in range(2):
+                entrants = rng.integers(0, len(population), config.tournament_size)
+                winner = min(entrants, key=lambda i: (costs[i], i))
+                parents.append(population[int(winner)])
+            mother, father = parents
+            if L > 1 and rng.random() < config.crossover_rate:
+                point = int(rng.integers(1, L))
+                child = mother[:point] + father[point:]
+            else:
+                child = mother
+            genes = list(child)
+            for g in range(L):
+                if rng.random() < mutation_rate:
+                    genes[g] = int(rng.integers(0, T))
+            children.append(tuple(genes))
+        population = children
+        scored = evaluate_population(population)
+    return ScoredPlan(best.plan, best.provisioning, best.cost, best.report, scorer.evaluations)
+
+
+def heuristic_first_layer(graph, catalog, invert: bool = False) -> SchedulingPlan:
+    """First layer on the cheapest CPU type, the rest on the accelerator with the smallest
+    summed computation time; ``invert`` swaps the roles (ls/baselines.py:190-219)."""
+    cpu = catalog.cheapest_cpu_type()
+    accelerators = [t for t in catalog.types if not t.is_cpu]
+
+    def best_accel(layers) -> int:
+        if not accelerators:
+            raise ConfigError("heuristic needs at least one accelerator type")
+        return min(accelerators,
+                   key=lambda t: (sum(l.per_type_oct[t.id] for l in layers), t.id)).id
+
+    if not invert:
+        if graph.num_layers == 1:
+            return SchedulingPlan((cpu.id,))
+        gpu = best_accel(graph.layers[1:])
+        return SchedulingPlan((cpu.id,) + (gpu,) * (graph.num_layers - 1))
+    gpu = best_accel(graph.layers[:1])
+    return SchedulingPlan((gpu,) + (cpu.id,) * (graph.num_layers - 1))
+
+
+def homogeneous(graph, catalog, type_id: int) -> SchedulingPlan:
+    """Every layer on one type (ls/baselines.py:222-228)."""
+    if not 0 <= type_id < catalog.num_types:
+        raise PlanValidationError(f"unknown type id {type_id} (catalog has "
+                                  f"{catalog.num_types} types)")
+    return SchedulingPlan((type_id,) * graph.num_layers)
+
+
+__all__ = ["brute_force", "random_search", "greedy", "genetic", "GeneticConfig",
+           "heuristic_first_layer", "homogeneous", "enumerate_argmin", "allgather_argmin", "merge_keys",
            "shard_range", "decode_index", "decode_packed", "DEFAULT_ENUMERATION_CAP"]
