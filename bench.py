@@ -200,24 +200,26 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_2111_10635_b200 import _abi
     from paper_2111_10635_b200.instance import DeviceInstance
-    from paper_2111_10635_b200.search import (allgather_argmin, brute_force, merge_keys,
-                                              shard_range)
+    from paper_2111_10635_b200.search import (allgather_argmin, brute_force, enum_shard_async,
+                                              merge_keys, shard_range, shard_strided)
 
     rank, world, local = dist_env()
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"   # NCCL's banner goes to stdout: keep ONE JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     g, c, job = instance()
     T, L = c.num_types, g.num_layers
     total = T ** L
-    lo, hi = shard_range(0, total, rank, world)
+    my_plans = shard_strided(0, total, rank, world)[2]  # every world-th index (balanced)
     inst = DeviceInstance(g, c, job)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def sweep():
-        return allgather_argmin(inst.enum_argmin_async(lo, hi, True))
+        return allgather_argmin(enum_shard_async(inst, 0, total, rank, world, True))
 
     for _ in range(max(3, args.warmup)):
         key = sweep()
@@ -231,7 +233,7 @@ def run_ours(args):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            buf = inst.enum_argmin_async(lo, hi, True)
+            buf = enum_shard_async(inst, 0, total, rank, world, True)
             e1.record()
             keys.append(allgather_argmin(buf))  # the exchange (and its host read) follows
             torch.cuda.synchronize()
@@ -240,6 +242,12 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     my_total = sum(step_ms)
+    per_rank_ms = [my_total / args.steps]
+    if world > 1:   # diagnostic: every rank's mean step time (the value uses the max)
+        pr = torch.zeros(world, dtype=torch.float64, device=dev)
+        pr[rank] = my_total / args.steps
+        dist.all_reduce(pr)
+        per_rank_ms = [float(x) for x in pr.cpu()]
     t = torch.tensor([my_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -334,7 +342,7 @@ def run_ours(args):
 
     if rank == 0:
         peak = fp64_peak(torch, inst.lib, dev)
-        kernel_plans_per_s = (hi - lo) / (statistics.median(step_ms) * 1e-3)
+        kernel_plans_per_s = my_plans / (statistics.median(step_ms) * 1e-3)
         achieved = kernel_plans_per_s * W_REF_OPS / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -356,6 +364,7 @@ def run_ours(args):
                                  f"FP64 ops per plan ({W_REF_OPS}, SURVEY.md §8(d)); peak = DFMA "
                                  "probe measured in this run (MEASURED_PEAKS.json has no FP64)"},
             "clocks": clocks.summary(),
+            "per_rank_ms": per_rank_ms,
         }
         if rl is not None:
             line["rl"] = rl

@@ -157,6 +157,13 @@ int hps_plans_argmin(HpsInstance* inst, const uint8_t* d_plans, int64_t n, int32
 int hps_random_argmin(HpsInstance* inst, const HpsPcg64* gen, uint64_t first, uint64_t n,
                       HpsArgmin* d_best, void* stream);
 
+/* hps_enum_argmin over the arithmetic progression first, first + stride, ... (count indices):
+ * rank r of W takes (first = begin + r, stride = W), which deals neighbouring plans — whose
+ * provisioning work is correlated — to different GPUs and balances the shards. Same key
+ * semantics as hps_enum_argmin (the rank field is the enumeration index). */
+int hps_enum_argmin_strided(HpsInstance* inst, uint64_t first, uint64_t stride, uint64_t count,
+                            int32_t feasible_only, HpsArgmin* d_best, void* stream);
+
 /* Materialise the random plans of hps_random_argmin into d_plans (u8 [n][L]). */
 int hps_random_plans(HpsInstance* inst, const HpsPcg64* gen, uint64_t first, uint64_t n,
                      uint8_t* d_plans, void* stream);

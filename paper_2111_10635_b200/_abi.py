@@ -154,6 +154,8 @@ _SIGNATURES = {
     "hps_policy_last_error": (C.c_char_p, []),
     "hps_probe_fp64": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "hps_stats_read": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "hps_enum_argmin_strided": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                          C.c_int32, C.c_void_p, C.c_void_p]),
     "hps_score_plans_static": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                          C.c_void_p, C.c_void_p]),
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),

@@ -54,6 +54,7 @@ struct PlanSource {
   int32_t tbits;         // mode 2: log2(T)
   const uint8_t* plans;  // mode 0
   uint64_t begin;        // mode 1/2: first enumeration index / first random plan
+  uint64_t stride;       // mode 1: plan p is enumeration index begin + p * stride
   uint64_t tpow[kMaxL];  // mode 1: T^(L-1-l)
   // mode 2: state after (first*L/2 + 1) steps is computed per warp; A_j/C_j advance it by j
   uint64_t s0_hi, s0_lo, inc_hi, inc_lo;
@@ -89,7 +90,7 @@ __device__ __forceinline__ void load_digits(const InstanceConsts& c, const PlanS
       rank = mk(hi, lo);
     }
   } else if (MODE == 1) {
-    const uint64_t idx = src.begin + p;
+    const uint64_t idx = src.begin + p * src.stride;
     if (idx < 0xffffffffull && src.tpow[0] < 0xffffffffull) {  // 32-bit division is much cheaper
       const uint32_t i32 = (uint32_t)idx, t32 = (uint32_t)c.T;
       if (lane < L) d0 = (int)((i32 / (uint32_t)src.tpow[lane]) % t32);
@@ -1020,6 +1021,15 @@ struct ArgminScratch {
 
 int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_only, HpsArgmin* d_best,
                   cudaStream_t st) {
+  if (n == 0) {   // empty range: the identity key (cost +inf, nothing evaluated)
+    unsigned int* zero = nullptr;
+    CUDA_TRY(cudaMallocAsync(&zero, sizeof(unsigned int), st));
+    CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(unsigned int), st));
+    finish_argmin<<<1, 256, 0, st>>>(nullptr, 0, nullptr, zero, 0, 0, d_best);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(zero, st));
+    return HPS_OK;
+  }
   const int grid = grid_for(in, n);
   const int nparts = grid * warps_per_block(in) * (in->fast ? 2 : 1);
   const unsigned cap = (unsigned)std::min<uint64_t>(kSlowCap, std::max<uint64_t>(n, 1));
@@ -1220,9 +1230,28 @@ int hps_enum_argmin(HpsInstance* in, uint64_t begin, uint64_t end, int32_t feasi
   PlanSource src{};
   src.mode = 1;
   src.begin = begin;
+  src.stride = 1;
   uint64_t pw = 1;
   for (int l = in->c.L - 1; l >= 0; l--) { src.tpow[l] = pw; pw *= (uint64_t)in->c.T; }
   return argmin_common(in, src, end - begin, feasible_only, d_best, (cudaStream_t)stream);
+}
+
+int hps_enum_argmin_strided(HpsInstance* in, uint64_t first, uint64_t stride, uint64_t count,
+                            int32_t feasible_only, HpsArgmin* d_best, void* stream) {
+  if (!in || !d_best || stride == 0) return set_err(HPS_E_INVALID_ARG, "bad stride");
+  long double total = powl((long double)in->c.T, (long double)in->c.L);
+  if (total > 1.8e19L) return set_err(HPS_E_CONFIG, "T^L does not fit a 64-bit enumeration index");
+  uint64_t tot = 1;
+  for (int l = 0; l < in->c.L; l++) tot *= (uint64_t)in->c.T;
+  if (count > 0 && (first >= tot || (count - 1) > (tot - 1 - first) / stride))
+    return set_err(HPS_E_INVALID_ARG, "strided range beyond T^L");
+  PlanSource src{};
+  src.mode = 1;
+  src.begin = first;
+  src.stride = stride;
+  uint64_t pw = 1;
+  for (int l = in->c.L - 1; l >= 0; l--) { src.tpow[l] = pw; pw *= (uint64_t)in->c.T; }
+  return argmin_common(in, src, count, feasible_only, d_best, (cudaStream_t)stream);
 }
 
 int hps_plans_argmin(HpsInstance* in, const uint8_t* d_plans, int64_t n, int32_t feasible_only,

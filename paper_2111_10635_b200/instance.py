@@ -121,6 +121,16 @@ class DeviceInstance:
                                                 _ptr(buf), _stream(stream)), "hps_enum_argmin")
         return buf
 
+    def enum_argmin_strided_async(self, first: int, stride: int, count: int,
+                                  feasible_only: bool = True, stream=None):
+        buf = self._argmin_buffer()
+        with torch.cuda.device(self.device):
+            _abi.check(self.lib.hps_enum_argmin_strided(self.handle, first, stride, count,
+                                                        1 if feasible_only else 0, _ptr(buf),
+                                                        _stream(stream)),
+                       "hps_enum_argmin_strided")
+        return buf
+
     def plans_argmin_async(self, plans, feasible_only: bool = False, stream=None):
         plans = plans.to(self.device).contiguous()
         buf = self._argmin_buffer()

@@ -28,7 +28,10 @@ def _worker(r, world, port, keys, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=r, world_size=world)
     try:
-        merged = allgather_argmin(_key_bytes(*keys[r]))
+        kr = keys[r]
+        buf = (torch.cat([_key_bytes(*k) for k in kr]) if isinstance(kr, list)
+               else _key_bytes(*kr))
+        merged = allgather_argmin(buf)
         out_q.put((r, merged))
     finally:
         dist.destroy_process_group()
@@ -38,6 +41,8 @@ def _worker(r, world, port, keys, out_q):
     ([(0.5, 10, 100, 7), (0.25, 99, 100, 3)], (0.25, 99, 200, 10)),
     ([(0.25, 12, 50, 1), (0.25, 7, 50, 2)], (0.25, 7, 100, 3)),        # cost tie -> smaller rank
     ([(float("inf"), 2 ** 64 - 1, 10, 0), (1.5, 2 ** 100 + 5, 10, 1)], (1.5, 2 ** 100 + 5, 20, 1)),
+    # several keys per rank in one buffer
+    ([[(0.5, 1, 5, 1), (0.3, 40, 5, 2)], [(0.3, 17, 5, 3), (0.9, 60, 5, 4)]], (0.3, 17, 20, 10)),
 ])
 def test_allgather_argmin_gloo_world2(keys, expect):
     ctx = mp.get_context("spawn")

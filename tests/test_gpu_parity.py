@@ -115,6 +115,14 @@ def test_enum_argmin_cfg4_full_and_shards():
              for r in range(8)]
     m = merge_keys(parts)
     assert (m["cost"], m["rank"], m["feasible"]) == (key["cost"], key["rank"], key["feasible"])
+    from paper_2111_10635_b200.search import enum_shard_async
+    for w in (3, 8):   # strided shards, merged like the multi-GPU path
+        keys = [inst.read_argmin(enum_shard_async(inst, 0, 2 ** 16, r, w)) for r in range(w)]
+        m = merge_keys(keys)
+        assert (m["cost"], m["rank"], m["feasible"], m["evaluated"]) == \
+            (key["cost"], key["rank"], key["feasible"], 2 ** 16)
+    e = inst.read_argmin(inst.enum_argmin_async(5, 5, True))   # empty piece = identity key
+    assert e["cost"] == float("inf") and e["evaluated"] == 0 and e["feasible"] == 0
 
 
 def test_brute_force_dropin_matches_reference_winners():

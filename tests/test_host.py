@@ -54,6 +54,19 @@ def test_shards_cover_range_exactly():
         assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
 
 
+def test_strided_shards_partition_range():
+    from paper_2111_10635_b200.search import shard_strided
+    for b, n, w in [(0, 3 ** 16, 8), (0, 3 ** 16, 4), (7, 100, 3), (0, 5, 8), (3, 1, 2)]:
+        got = []
+        for r in range(w):
+            first, stride, count = shard_strided(b, b + n, r, w)
+            got += [first + j * stride for j in range(min(count, 50000))]
+        if n <= 50000:
+            assert sorted(got) == list(range(b, b + n))
+        else:
+            assert sum(shard_strided(b, b + n, r, w)[2] for r in range(w)) == n
+
+
 def test_merge_keys_is_deterministic_min():
     keys = [{"cost": 2.0, "rank": 5, "evaluated": 10, "feasible": 3, "flags": 0, "status": 0},
             {"cost": 1.0, "rank": 9, "evaluated": 10, "feasible": 4, "flags": 0, "status": 0},
