@@ -711,6 +711,8 @@ struct HpsInstance {
   bool fast = false;
   std::vector<StageEntry> h_stages;
   int sm_count = 148;
+  int grid_per_sm = 16;   // blocks per SM of the split kernels' grid (HPS_GRID_PER_SM)
+  int carveout = -1;      // shared-memory carveout % for the split kernels (HPS_CARVEOUT)
 };
 
 namespace {
@@ -922,6 +924,7 @@ int launch_stage(HpsInstance* in, const PlanSource& src, uint64_t p0, uint64_t p
   const size_t smem = sizeof(WarpSmem<MAXS>) * WARPS;
   auto kern = stage_kernel<MAXS, WARPS, ARGMIN, SRC>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
   kern<<<grid, WARPS * 32, smem, st>>>(in->c, in->tb, src, p0, p1, o, pend, cont, feasible_only, parts, first);
   CUDA_TRY(cudaGetLastError());
   return HPS_OK;
@@ -940,6 +943,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   const size_t smem2 = (sizeof(WarpSmem<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
   for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
     const uint64_t c1 = std::min(n, c0 + chunk);
     const int first = (c0 == 0);
@@ -967,7 +971,7 @@ int dispatch_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Out
 int grid_for(HpsInstance* in, uint64_t n_plans) {
   const int warps = warps_per_block(in);
   uint64_t blocks = (n_plans + warps - 1) / warps;
-  uint64_t cap = (uint64_t)in->sm_count * 16;
+  uint64_t cap = (uint64_t)in->sm_count * in->grid_per_sm;
   return (int)std::max<uint64_t>(1, std::min(blocks, cap));
 }
 
@@ -1087,6 +1091,8 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   CUDA_TRY(cudaGetDevice(&dev));
   auto* in = new HpsInstance();
   cudaDeviceGetAttribute(&in->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (const char* e = getenv("HPS_GRID_PER_SM")) in->grid_per_sm = std::max(1, atoi(e));
+  if (const char* e = getenv("HPS_CARVEOUT")) in->carveout = std::min(100, atoi(e));
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {

@@ -22,13 +22,18 @@
 
 namespace hps {
 
+#ifndef HPS_TOP
+#define HPS_TOP 2
+#endif
+constexpr int kTop = HPS_TOP;   // unpinned stages bounded individually by cost_bound
+
 template <int MAXS>
 struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase (broadcast reads)
   double pr[MAXS];   // price per second of stage r's type
   double etp[MAXS];  // exact et at the pinned count (kmin == kmax), else unused
   double pmin_rest;  // sum over non-top stages of price * kmin, rounded down by 1e-13
   double ep_max;     // max over pinned stages of their exact et
-  int32_t top[2];    // unpinned stages with the largest price-weighted count span (-1: none)
+  int32_t top[kTop]; // unpinned stages with the largest price-weighted count span (-1: none)
   double q[64];      // survivors of the lower-bound filter, evaluated 32 at a time
 };
 
@@ -79,7 +84,7 @@ __device__ __forceinline__ double cost_bound(const CostScalars cs, const WarpSme
   const float tf = (float)tau;
   float P = (float)sw.pmin_rest, E = (float)sw.ep_max;
 #pragma unroll
-  for (int q = 0; q < 2; q++) {
+  for (int q = 0; q < kTop; q++) {
     const int r = sw.top[q];
     if (r < 0) continue;
     int kl, ku;
@@ -123,19 +128,32 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   }
   __syncwarp();
   if (lane == 0) {
-    int t0 = -1, t1 = -1;
-    double v0 = -1.0, v1 = -1.0, ep = 0.0;
+    int t[kTop];
+    double v[kTop];
+#pragma unroll
+    for (int q = 0; q < kTop; q++) { t[q] = -1; v[q] = -1.0; }
+    double ep = 0.0;
     for (int r = 0; r < S; r++) {
       if (w.kmax[r] == w.kmin[r]) { ep = fmax(ep, sw.etp[r]); continue; }
-      const double v = sw.pr[r] * (w.kmax[r] - w.kmin[r]);
-      if (v > v0) { v1 = v0; t1 = t0; v0 = v; t0 = r; }
-      else if (v > v1) { v1 = v; t1 = r; }
+      double vv = sw.pr[r] * (w.kmax[r] - w.kmin[r]);
+      int tt = r;
+#pragma unroll
+      for (int q = 0; q < kTop; q++) {   // insertion into the descending top list
+        if (vv > v[q]) {
+          const double v2 = v[q]; const int t2 = t[q];
+          v[q] = vv; t[q] = tt; vv = v2; tt = t2;
+        }
+      }
     }
     double pm = 0.0;
-    for (int r = 0; r < S; r++)
-      if (r != t0 && r != t1) pm += sw.pr[r] * w.kmin[r];
-    sw.top[0] = t0;
-    sw.top[1] = t1;
+    for (int r = 0; r < S; r++) {
+      bool in_top = false;
+#pragma unroll
+      for (int q = 0; q < kTop; q++) in_top |= (t[q] == r);
+      if (!in_top) pm += sw.pr[r] * w.kmin[r];
+    }
+#pragma unroll
+    for (int q = 0; q < kTop; q++) sw.top[q] = t[q];
     sw.pmin_rest = pm * (1.0 - 1e-13);
     sw.ep_max = ep;
     HPS_STAT(ST_NCAND, n_cand);
