@@ -37,6 +37,7 @@ UNIT = "plans/s"
 # reference-algorithm FP64 operations per plan on cfg3 (24*E[S*C] + 9*N_bp +
 # 13*61*S + 4*C + 88*L + 60*S with the measured means E[S*C]=7718, N_bp=697, S=11, C=689)
 W_REF_OPS = 205_052
+TRAFFIC_BYTES_PER_PLAN = 849   # ncu dram__bytes_{read,write}.sum over a cfg3 sweep / plans
 
 
 def parse():
@@ -359,10 +360,16 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": 3 * args.steps * world,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "note": "achieved = plans/s of the sweep kernel x reference-algorithm "
-                                 f"FP64 ops per plan ({W_REF_OPS}, SURVEY.md §8(d)); peak = DFMA "
-                                 "probe measured in this run (MEASURED_PEAKS.json has no FP64)"},
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": TRAFFIC_BYTES_PER_PLAN * my_plans,
+                         "note": "achieved = plans/s of the sweep (stage + candidate + slow "
+                                 "kernels, one step) x reference-algorithm FP64 ops per plan "
+                                 f"({W_REF_OPS}, SURVEY.md §8(d)); peak = DFMA probe measured in "
+                                 "this run (MEASURED_PEAKS.json has no FP64); traffic = DRAM "
+                                 f"bytes per step at {TRAFFIC_BYTES_PER_PLAN} B/plan from the ncu "
+                                 "launch list (profiles/r1_launches_bench_v18_summary.txt): "
+                                 "the split kernels' per-plan state round trip, <1% of HBM "
+                                 "bandwidth at this rate"},
             "clocks": clocks.summary(),
             "per_rank_ms": per_rank_ms,
         }
