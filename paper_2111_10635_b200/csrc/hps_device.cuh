@@ -117,15 +117,61 @@ static __device__ HPS_NOINLINE_RARE int count_cert(const StageEntry& s, double t
   return c_lo < 1.0 ? 1 : (int)c_lo;
 }
 
+// count_cert for a stage whose count is decided by ONE side (see side_dominance): the same
+// certified arithmetic on that side only.
+static __device__ HPS_NOINLINE_RARE int count_cert1(double frac, double omf, double rw, double tau,
+                                                    double bo) {
+  const double B = (tau * bo) * rw;
+  const double h = B - omf;
+  const double eh = (4.0 * B + 3.0 * fabs(h)) * 1.1102230246251565e-16;
+  HPS_STAT(ST_CERT, 1);
+  if (!(h > 2.0 * eh)) { HPS_STAT(ST_CERT_FAIL, 1); return -1; }
+  const double rh = rcp_1nt(h);
+  const double q = frac * rh;
+  const double dq = q * fma(2.02 * eh, rh, 1.0e-12);
+  const double c_lo = ceil(dmax_nn(1.0, q - dq) - 1e-9), c_hi = ceil(dmax_nn(1.0, q + dq) - 1e-9);
+  if (c_lo != c_hi || !(c_hi < 2.0e9)) { HPS_STAT(ST_CERT_FAIL, 1); return -1; }
+  return (int)c_lo;
+}
+
+// Which side of _floor_count (ls/provisioner.py:150-176) decides a stage's count for every tau
+// in [tlo, thi]: 1 = computation, 2 = communication, 0 = undecided (use both). With both
+// sides active, q_o - q_d = N / (h_o h_d) with N = alpha h_d - beta h_o LINEAR in tau, so a
+// sign of N that holds with margin at both ends holds on the whole interval; the margin
+// (relative 1e-9, far above the rounding of h and q) makes the reference's rounded q's obey
+// the same order, and iceil is monotone, so max(iceil(q_o), iceil(q_d)) = iceil(q_dominant).
+__device__ __forceinline__ int side_dominance(const StageEntry& s, double tlo, double thi, double bo) {
+  if (s.odt == 0.0) return (s.oct != 0.0 && s.alpha > 0.0) ? 1 : 0;
+  if (s.oct == 0.0) return (s.beta > 0.0) ? 2 : 0;
+  if (!(s.alpha > 0.0) || !(s.beta > 0.0)) return 0;
+  int sg[2];
+#pragma unroll
+  for (int e = 0; e < 2; e++) {
+    const double A = (e ? thi : tlo) * bo;
+    const double Bo = A * s.rwo, Bd = A * s.rwd;
+    const double ho = Bo - s.oma, hd = Bd - s.omb;
+    const double eo = (4.0 * Bo + 3.0 * fabs(ho)) * 1.1102230246251565e-16;
+    const double ed = (4.0 * Bd + 3.0 * fabs(hd)) * 1.1102230246251565e-16;
+    if (!(ho > 2.0 * eo) || !(hd > 2.0 * ed)) return 0;
+    const double N = s.alpha * hd - s.beta * ho;
+    const double M = 8.0 * (s.alpha * ed + s.beta * eo) + 1e-9 * (s.alpha * hd + s.beta * ho);
+    sg[e] = (N > M) ? 1 : ((N < -M) ? 2 : 0);
+  }
+  return (sg[0] == sg[1]) ? sg[0] : 0;
+}
+
 // One-sided count bounds in FP32 for pruning only: returns lower bound kl <= count(tau) and
 // upper bound ku >= count(tau) (ku = 0 when no bound could be established). Relative error of
 // every FP32 quantity is bounded by a few 2^-24; with kappa = B/h the headroom's relative
 // error is <= 3e-7 (kappa + 1), so q in q~ (1 +- 4e-7 (kappa + 2)). floor(q_lo) <= ceil(q - 1e-9).
-__device__ __forceinline__ void count_bounds32(const StageEntry& s, float tau, int& kl, int& ku) {
+// dom (side_dominance) restricts the bound to the deciding side.
+__device__ __forceinline__ void count_bounds32(const StageEntry& s, float tau, int dom, int& kl,
+                                               int& ku) {
   float lo = 1.0f, hi = 1.0f;
   bool ok = true;
 #pragma unroll
   for (int side = 0; side < 2; side++) {
+    if (dom == 2 - side) continue;   // dom 1 skips side 1, dom 2 skips side 0
     const float rb = side ? s.f_rbd : s.f_rbo;
     if (rb == 0.0f) continue;  // work == 0
     const float frac = side ? s.f_beta : s.f_alpha;

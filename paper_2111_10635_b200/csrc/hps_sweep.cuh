@@ -34,13 +34,19 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   double pmin_rest;  // sum over non-top stages of price * kmin, rounded down by 1e-13
   double ep_max;     // max over pinned stages of their exact et
   int32_t top[kTop]; // unpinned stages with the largest price-weighted count span (-1: none)
+  int32_t dom[MAXS]; // side_dominance over [tau_lo, tau_hi]: 1 oct, 2 odt, 0 both
   double q[64];      // survivors of the lower-bound filter, evaluated 32 at a time
 };
 
-// exact count at tau in [tau_lo, tau_hi] (count in [kmin, kmax]): certified, table fallback
+// exact count at tau in [tau_lo, tau_hi] (count in [kmin, kmax]): certified (one side when it
+// provably dominates), table fallback
 template <int MAXS>
-__device__ __forceinline__ int count_fast(double bo, const WarpSmem<MAXS>& w, int r, double tau) {
-  const int k = count_cert(w.st[r], tau, bo);
+__device__ __forceinline__ int count_fast(double bo, const WarpSmem<MAXS>& w, int r, double tau,
+                                          int dom) {
+  const StageEntry& s = w.st[r];
+  const int k = (dom == 1)   ? count_cert1(s.alpha, s.oma, s.rwo, tau, bo)
+                : (dom == 2) ? count_cert1(s.beta, s.omb, s.rwd, tau, bo)
+                             : count_cert(s, tau, bo);
   if (k > 0) return k;
   return count_tab(w.row[r], tau, (int)w.kmin[r], (int)w.kmax[r], est_count(w.st[r], tau));
 }
@@ -63,7 +69,7 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<M
       k = (int)w.kmin[r];
       et = sw.etp[r];
     } else {
-      k = count_fast<MAXS>(cs.bo, w, r, tau);
+      k = count_fast<MAXS>(cs.bo, w, r, tau, sw.dom[r]);
       et = w.row[r][k - 1].et;
     }
     E = (r == 0) ? et : fmax(E, et);
@@ -88,7 +94,7 @@ __device__ __forceinline__ double cost_bound(const CostScalars cs, const WarpSme
     const int r = sw.top[q];
     if (r < 0) continue;
     int kl, ku;
-    count_bounds32(w.st[r], tf, kl, ku);
+    count_bounds32(w.st[r], tf, sw.dom[r], kl, ku);
     const int lo = (int)w.kmin[r], hi = (int)w.kmax[r];
     kl = max(kl, lo);
     P += (float)sw.pr[r] * (float)kl;
@@ -125,6 +131,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   for (int r = lane; r < S; r += 32) {
     sw.pr[r] = c.price_s[w.st[r].type];
     sw.etp[r] = (w.kmax[r] == w.kmin[r]) ? w.row[r][(int)w.kmin[r] - 1].et : 0.0;
+    sw.dom[r] = (w.kmax[r] == w.kmin[r]) ? 0 : side_dominance(w.st[r], tau_lo, tau_hi, c.bo);
   }
   __syncwarp();
   if (lane == 0) {
@@ -212,6 +219,18 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   const double mf = warp_min(buf.mn);
   if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
   const double lim = mf + 1e-15;
+#ifdef HPS_STATS
+  {  // diagnostics: survivors the filter would keep with the final minimum as its bound
+    int sp2 = 0, ideal = 0, unp = 0;
+    for (int i = lane; i < n_cand; i += 32) {
+      const double tau = cand_tau<MAXS>(w, i, sp2, tau_lo, tau_hi);
+      if (tau >= tau_lo && tau <= tau_hi && !(cost_bound<MAXS>(cs, w, sw, tau) > lim)) ideal++;
+    }
+    for (int r = lane; r < S; r += 32) unp += (w.kmax[r] != w.kmin[r]);
+    HPS_STAT(ST_CHUNKS, ideal);
+    HPS_STAT(ST_UNPINNED, unp);
+  }
+#endif
   double bt;
   if (__any_sync(0xffffffffu, buf.overflow)) {  // rare: exact second pass with the final limit
     bt = -inf;
