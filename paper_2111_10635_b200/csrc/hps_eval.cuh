@@ -192,11 +192,16 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
   }
   bool closed = false;
   double tstar_single = 0.0;
+  int n_unres = -1;   // unresolved stages when the closed-form test last ran
   for (; it < 60; it++) {
     // (1) each type has at most one unresolved stage r: on (a, b) its type's constraint is
     //     count_r(mid) <= K_r = Q_t - sum of the type's other (pinned) counts, i.e.
     //     mid >= theta_r(K_r); quota_ok switches at the max of those thresholds.
-    {
+    //     The test can only change outcome when a stage got resolved since it last ran.
+    const int n_now = __popc(__ballot_sync(0xffffffffu, ty[0] >= 0 && ub[0] != lb[0])) +
+                      __popc(__ballot_sync(0xffffffffu, ty[1] >= 0 && ub[1] != lb[1]));
+    if (n_now != n_unres) {
+      n_unres = n_now;
       const bool u0 = ty[0] >= 0 && ub[0] != lb[0], u1 = ty[1] >= 0 && ub[1] != lb[1];
       const unsigned tm = (u0 ? 1u << ty[0] : 0u) | (u1 ? 1u << ty[1] : 0u);
       const unsigned types_u = __reduce_or_sync(0xffffffffu, tm);
