@@ -7,7 +7,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-NAMES = ["plans", "ideal_survivors", "slow_overflow", "cands_eval", "probes_exact", "probes_closed", "cert",
+NAMES = ["plans", "ideal_survivors", "unused", "cands_eval", "probes_exact", "probes_closed", "cert",
          "cert_fail", "tab", "pending", "stages", "unpinned", "ncand", "plans_fast", "cyc_stages_bisect", "cyc_candidates",
          "cyc_final", "cyc_pass1", "cyc_pass2"]
 
