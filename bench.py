@@ -229,6 +229,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     step_ms = []
     keys = []
+    launches0 = inst.lib.hps_launch_count()
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()
@@ -239,6 +240,7 @@ def run_ours(args):
             keys.append(allgather_argmin(buf))  # the exchange (and its host read) follows
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
+    my_launches = inst.lib.hps_launch_count() - launches0   # this rank's kernels, timed region
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -253,6 +255,10 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
+    nl = torch.tensor([my_launches], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(nl)
+    gpu_launches = int(nl.item())   # summed over ranks
     value = total * args.steps / (total_ms * 1e-3)
     key = keys[-1]
     assert all(k["rank"] == key["rank"] and k["cost"] == key["cost"] for k in keys)
@@ -358,7 +364,7 @@ def run_ours(args):
                        "feasible_plans": key["feasible"]},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": 3 * args.steps * world,
+            "gpu_launches": gpu_launches,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": TRAFFIC_BYTES_PER_PLAN * my_plans,

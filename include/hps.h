@@ -213,6 +213,10 @@ int hps_policy_reinforce(HpsPolicy* policy, const double* d_cost, const uint8_t*
 int hps_policy_state(HpsPolicy* policy, double* state3, int32_t* flags2);
 const char* hps_policy_last_error(void);
 
+/* Number of kernels this library has launched in the process (all entry points, host-side
+ * counter incremented at every launch). bench.py reports the difference over its timed region. */
+uint64_t hps_launch_count(void);
+
 /* Device counters of an instrumented build (-DHPS_STATS); HPS_E_CONFIG otherwise. */
 int hps_stats_read(unsigned long long* out, int n, int reset);
 

@@ -156,6 +156,7 @@ _SIGNATURES = {
     "hps_stats_read": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "hps_enum_argmin_strided": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                           C.c_int32, C.c_void_p, C.c_void_p]),
+    "hps_launch_count": (C.c_uint64, []),
     "hps_score_plans_static": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                          C.c_void_p, C.c_void_p]),
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),

@@ -10,6 +10,7 @@
 //   K7         slow_kernel        block per plan for the >4096-breakpoint path: sort, dedup,
 //                                 Newton/golden + subsample (ls/provisioner.py:456-470)
 //   reduce     finish_argmin      deterministic merge of per-block keys
+#include "hps_launch.h"
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -893,6 +894,7 @@ int launch_eval(HpsInstance* in, const PlanSource& src, uint64_t n, const Output
   const size_t smem = sizeof(WarpSmem<MAXS>) * WARPS + (FAST ? sizeof(SweepSmem<MAXS>) * WARPS : 0);
   auto kern = eval_kernel<MAXS, WARPS, ARGMIN, FAST, SRC>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HPS_COUNT_LAUNCH();
   kern<<<grid, WARPS * 32, smem, st>>>(in->c, in->tb, src, n, o, pend, feasible_only, parts);
   CUDA_TRY(cudaGetLastError());
   return HPS_OK;
@@ -925,6 +927,7 @@ int launch_stage(HpsInstance* in, const PlanSource& src, uint64_t p0, uint64_t p
   auto kern = stage_kernel<MAXS, WARPS, ARGMIN, SRC>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
+  HPS_COUNT_LAUNCH();
   kern<<<grid, WARPS * 32, smem, st>>>(in->c, in->tb, src, p0, p1, o, pend, cont, feasible_only, parts, first);
   CUDA_TRY(cudaGetLastError());
   return HPS_OK;
@@ -953,6 +956,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     else if (src.mode == 1) rc = launch_stage<MAXS, WARPS, ARGMIN, 1>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     if (rc) return rc;
+    HPS_COUNT_LAUNCH();
     k2<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, o, feasible_only, parts_b, first);
     CUDA_TRY(cudaGetLastError());
   }
@@ -989,6 +993,7 @@ int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending p
   const size_t cap_blocks = std::max<size_t>(8, ((size_t)4 << 30) / (per_block * sizeof(double)));
   const int blocks = (int)std::min<size_t>((size_t)in->sm_count * 2, cap_blocks);
   CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
+  HPS_COUNT_LAUNCH();
   slow_kernel<<<blocks, kSlowThreads, 0, st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
                                                     slow_parts, scratch, per_block);
   CUDA_TRY(cudaGetLastError());
@@ -1029,6 +1034,7 @@ int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_onl
     unsigned int* zero = nullptr;
     CUDA_TRY(cudaMallocAsync(&zero, sizeof(unsigned int), st));
     CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(unsigned int), st));
+    HPS_COUNT_LAUNCH();
     finish_argmin<<<1, 256, 0, st>>>(nullptr, 0, nullptr, zero, 0, 0, d_best);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(zero, st));
@@ -1052,6 +1058,7 @@ int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_onl
   if (rc) return rc;
   rc = run_slow(in, src, o, pend, 1, feasible_only, slow_parts, st);
   if (rc) return rc;
+  HPS_COUNT_LAUNCH();
   finish_argmin<<<1, 256, 0, st>>>(parts, nparts, slow_parts, count, cap, n, d_best);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(buf, st));
@@ -1148,12 +1155,15 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   CUDA_TRY(cudaMalloc(&in->d_stage0, sizeof(Stage0Info) * T * L));
   CUDA_TRY(cudaMalloc(&in->d_te, sizeof(TEPair) * off));
   CUDA_TRY(cudaMalloc(&in->d_cls, sizeof(int32_t) * ne));
+  HPS_COUNT_LAUNCH();
   stage_table_kernel<<<(ne + 127) / 128, 128>>>(c, raw, in->d_stages);
   CUDA_TRY(cudaGetLastError());
+  HPS_COUNT_LAUNCH();
   stage0_kernel<<<(T * L + 127) / 128, 128>>>(c, in->d_stages, in->d_stage0);
   CUDA_TRY(cudaGetLastError());
   for (int t = 0; t < T; t++) {
     const int64_t cnt = (int64_t)c.P * (c.et_cap[t] + 1);
+    HPS_COUNT_LAUNCH();
     te_table_kernel<<<(unsigned)((cnt + 127) / 128), 128>>>(c, in->d_stages, in->d_te, t, cnt, c.te_off[t]);
     CUDA_TRY(cudaGetLastError());
   }
@@ -1349,6 +1359,10 @@ __global__ void report_kernel(const InstanceConsts c, const DeviceTables tb, con
 }
 }  // namespace
 
+std::atomic<unsigned long long> hps::g_launches{0};
+
+extern "C" uint64_t hps_launch_count(void) { return hps::g_launches.load(std::memory_order_relaxed); }
+
 extern "C" int hps_stats_read(unsigned long long* out, int n, int reset) {
 #ifdef HPS_STATS
   if (n > 24) n = 24;
@@ -1372,6 +1386,7 @@ extern "C" int hps_random_plans(HpsInstance* in, const HpsPcg64* g, uint64_t fir
   fill_random_source(in, g, first, src);
   if (n == 0) return HPS_OK;
   const uint64_t warps = std::min<uint64_t>(n, (uint64_t)in->sm_count * 64);
+  HPS_COUNT_LAUNCH();
   gen_plans_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(in->c, src, n, d_plans);
   CUDA_TRY(cudaGetLastError());
   return HPS_OK;
@@ -1383,6 +1398,7 @@ extern "C" int hps_report(HpsInstance* in, const uint8_t* d_plans, const int32_t
                           void* stream) {
   if (!in || n < 0) return set_err(HPS_E_INVALID_ARG, "bad argument");
   if (n == 0) return HPS_OK;
+  HPS_COUNT_LAUNCH();
   report_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       in->c, in->tb, d_plans, d_k, d_ps, n, d_ct, d_dt, d_et, d_tp, d_pipeline_tp, d_exec_time, d_cost, d_feasible);
   CUDA_TRY(cudaGetLastError());
@@ -1522,6 +1538,7 @@ extern "C" int hps_score_plans_static(HpsInstance* in, const uint8_t* d_plans, i
   if (cpu_per_gpu < 1) return set_err(HPS_E_INVALID_ARG, "cpu_per_gpu must be >= 1");
   if (n == 0) return HPS_OK;
   Outputs o{r->cost, r->status, r->gap, r->ps, r->num_stages, r->k};
+  HPS_COUNT_LAUNCH();
   static_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(in->c, in->tb, d_plans, n, mode,
                                                                                cpu_per_gpu, o);
   CUDA_TRY(cudaGetLastError());

@@ -9,6 +9,7 @@
 // summation order differs from OpenBLAS, so probabilities agree to ~1e-16 relative and sampled
 // plans are identical unless a uniform draw lands within that distance of a CDF boundary.
 // The hoisted input projection X @ W_x runs on the FP64 tensor cores (mma.sync m8n8k4 f64).
+#include "hps_launch.h"
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -497,10 +498,12 @@ int hps_policy_forward(HpsPolicy* p, double temperature, double* d_probs_out, vo
   cudaStream_t st = (cudaStream_t)stream;
   const PolicyDims& d = p->d;
   const int tiles = ((d.L + 7) / 8) * ((d.G4 + 7) / 8);
+  HPS_COUNT_LAUNCH();
   xw_dmma_kernel<<<(tiles * 32 + 127) / 128, 128, 0, st>>>(d, p->b.feat, p->b.w_cell, p->b.xw);
   PCUDA(cudaGetLastError());
   const int threads = ((d.G4 > d.T ? d.G4 : d.T) + 31) / 32 * 32;
   const size_t smem = sizeof(double) * (2 * d.H + d.G4 + d.T);
+  HPS_COUNT_LAUNCH();
   forward_kernel<<<1, threads, smem, st>>>(d, p->b, temperature);
   PCUDA(cudaGetLastError());
   if (d_probs_out)
@@ -514,6 +517,7 @@ int hps_policy_sample(HpsPolicy* p, const HpsPcg64* gen, uint64_t first_draw, in
   if (!p || !gen || !d_plans || n < 0) return perr(HPS_E_INVALID_ARG, "null argument");
   if (n == 0) return HPS_OK;
   const u128 s0 = ((u128)gen->state_hi << 64) | gen->state_lo, inc = ((u128)gen->inc_hi << 64) | gen->inc_lo;
+  HPS_COUNT_LAUNCH();
   sample_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(p->d, p->b.cdf, s0, inc,
                                                                                (u128)first_draw, n, d_plans);
   PCUDA(cudaGetLastError());
@@ -531,11 +535,14 @@ int hps_policy_reinforce(HpsPolicy* p, const double* d_cost, const uint8_t* d_st
   if (!p || G < 1) return perr(HPS_E_INVALID_ARG, "bad argument");
   cudaStream_t st = (cudaStream_t)stream;
   RoundIn in{d_cost, d_status, d_plans, G, temperature, lr, gamma, round, d_history, d_best_plan, d_best_where};
+  HPS_COUNT_LAUNCH();
   round_update_kernel<<<1, 256, 0, st>>>(p->d, p->b, in);
   PCUDA(cudaGetLastError());
   const size_t smem = sizeof(double) * (3 * p->d.H + p->d.G4);
+  HPS_COUNT_LAUNCH();
   backward_kernel<<<1, 512, smem, st>>>(p->d, p->b);
   PCUDA(cudaGetLastError());
+  HPS_COUNT_LAUNCH();
   update_kernel<<<1, 1024, 0, st>>>(p->d, p->b, lr);
   PCUDA(cudaGetLastError());
   return HPS_OK;

@@ -1,5 +1,6 @@
 // hps_probe.cu — FP64 pipe microbenchmark used by bench.py for the roofline denominator
 // (MEASURED_PEAKS.json carries HBM and bf16 peaks only; the plan evaluator is FP64-bound).
+#include "hps_launch.h"
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -31,6 +32,7 @@ __global__ void ddiv_probe(double* out, int iters) {
 
 extern "C" int hps_probe_fp64(int kind, double* d_out, int blocks, int threads, int iters,
                               void* stream) {
+  HPS_COUNT_LAUNCH();
   if (kind == 0)
     dfma_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(d_out, iters);
   else

@@ -19,7 +19,7 @@ ROOT = Path(__file__).resolve().parent.parent
 def test_library_exports_every_header_symbol():
     lib = _abi.load_library()
     header = (ROOT / "include" / "hps.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(hps_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(hps_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     for name in declared:
         assert hasattr(lib, name), name
