@@ -160,36 +160,6 @@ __device__ __forceinline__ int side_dominance(const StageEntry& s, double tlo, d
   return (sg[0] == sg[1]) ? sg[0] : 0;
 }
 
-// One-sided count bounds in FP32 for pruning only: returns lower bound kl <= count(tau) and
-// upper bound ku >= count(tau) (ku = 0 when no bound could be established). Relative error of
-// every FP32 quantity is bounded by a few 2^-24; with kappa = B/h the headroom's relative
-// error is <= 3e-7 (kappa + 1), so q in q~ (1 +- 4e-7 (kappa + 2)). floor(q_lo) <= ceil(q - 1e-9).
-// dom (side_dominance) restricts the bound to the deciding side.
-__device__ __forceinline__ void count_bounds32(const StageEntry& s, float tau, int dom, int& kl,
-                                               int& ku) {
-  float lo = 1.0f, hi = 1.0f;
-  bool ok = true;
-#pragma unroll
-  for (int side = 0; side < 2; side++) {
-    if (dom == 2 - side) continue;   // dom 1 skips side 1, dom 2 skips side 0
-    const float rb = side ? s.f_rbd : s.f_rbo;
-    if (rb == 0.0f) continue;  // work == 0
-    const float frac = side ? s.f_beta : s.f_alpha;
-    const float omf = side ? s.f_omb : s.f_oma;
-    const float B = tau * rb;
-    const float h = B - omf;
-    if (frac == 0.0f) continue;  // contributes nothing (in range no raise)
-    if (!(h > 1e-3f * B)) { ok = false; continue; }  // too much cancellation: no upper bound
-    const float rh = rcp_approx_f32(h);
-    const float q = frac * rh;
-    const float e = 4e-7f * (B * rh + 2.0f) + 1e-6f;
-    lo = fmaxf(lo, q * (1.0f - e));
-    hi = fmaxf(hi, q * (1.0f + e));
-  }
-  kl = (int)floorf(lo);
-  ku = ok ? (int)ceilf(hi) + 1 : 0;
-}
-
 // et(k) approximately (k >= 1 integer): within ~4 ulp of _stage_et(s, k)
 __device__ __forceinline__ double et_approx(const StageEntry& s, double k) {
   const double rk = rcp_refined(k);
@@ -240,6 +210,8 @@ struct DeviceTables {
   const TEPair* te;           // TE[e][m-1], m = 1 .. et_cap[t] + 1 (same offsets, stride cap+1)
   const int32_t* cls;         // [T * P] ET-equivalence class: entries with bitwise-equal
                               // (oct, odt, alpha, beta) share counts and breakpoints
+  const int32_t* gex;         // [T * P] largest M with count(et(m)) == m for every m <= M:
+                              // theta(m) <= et(m) < theta(m - 1) (exact generator counts)
 };
 
 __device__ __forceinline__ int tb_class(const DeviceTables& tb, int e) { return __ldg(tb.cls + e); }

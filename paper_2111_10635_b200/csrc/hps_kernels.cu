@@ -698,6 +698,26 @@ __global__ void te_table_kernel(const InstanceConsts c, const StageEntry* st, TE
   te[off + idx] = p;
 }
 
+// Per entry: the largest M such that every breakpoint et(m), m in [1, M], has count exactly m
+// (theta(m) <= et(m) gives count <= m, et(m) < theta(m - 1) gives count >= m). A candidate
+// tau = et_r(m) with m <= M then pins stage r's count to m and E(tau) >= et_r(m) = tau, which the
+// candidate phase's bound uses. (Rounding can break it for large m: the prefix stops there.)
+__global__ void gen_exact_init_kernel(const InstanceConsts c, int32_t* gex, int t) {
+  const int pe = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pe < c.P) gex[t * c.P + pe] = c.et_cap[t];
+}
+__global__ void gen_exact_kernel(const InstanceConsts c, const TEPair* te, int32_t* gex, int t,
+                                 int64_t count) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  const int cap = c.et_cap[t];
+  const int64_t pe = idx / cap;
+  const int m = (int)(idx % cap) + 1;
+  const TEPair* row = te + c.te_off[t] + pe * (cap + 1);
+  const double et = row[m - 1].et;  // et(m); row[m - 1].th = theta(m - 1), row[m].th = theta(m)
+  if (!((row[m].th <= et) && (et < row[m - 1].th))) atomicMin(gex + t * c.P + pe, m - 1);
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -709,6 +729,7 @@ struct HpsInstance {
   Stage0Info* d_stage0 = nullptr;
   TEPair* d_te = nullptr;
   int32_t* d_cls = nullptr;
+  int32_t* d_gex = nullptr;
   bool fast = false;
   std::vector<StageEntry> h_stages;
   int sm_count = 148;
@@ -856,6 +877,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Outpu
       w.row[s] = tb.te + c.te_off[st.type] + (int64_t)(e - st.type * c.P) * (int64_t)(c.et_cap[st.type] + 1);
       w.kmin[s] = (double)ps.kmin[s];
       w.kmax[s] = (double)ps.kmax[s];
+      w.cls[s] = tb_class(tb, e);
     }
     for (int s = lane; s <= S; s += 32) w.pre[s] = ps.pre[s];
     __syncwarp();
@@ -1155,6 +1177,7 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   CUDA_TRY(cudaMalloc(&in->d_stage0, sizeof(Stage0Info) * T * L));
   CUDA_TRY(cudaMalloc(&in->d_te, sizeof(TEPair) * off));
   CUDA_TRY(cudaMalloc(&in->d_cls, sizeof(int32_t) * ne));
+  CUDA_TRY(cudaMalloc(&in->d_gex, sizeof(int32_t) * ne));
   HPS_COUNT_LAUNCH();
   stage_table_kernel<<<(ne + 127) / 128, 128>>>(c, raw, in->d_stages);
   CUDA_TRY(cudaGetLastError());
@@ -1165,6 +1188,15 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
     const int64_t cnt = (int64_t)c.P * (c.et_cap[t] + 1);
     HPS_COUNT_LAUNCH();
     te_table_kernel<<<(unsigned)((cnt + 127) / 128), 128>>>(c, in->d_stages, in->d_te, t, cnt, c.te_off[t]);
+    CUDA_TRY(cudaGetLastError());
+  }
+  for (int t = 0; t < T; t++) {
+    HPS_COUNT_LAUNCH();
+    gen_exact_init_kernel<<<(c.P + 127) / 128, 128>>>(c, in->d_gex, t);
+    CUDA_TRY(cudaGetLastError());
+    const int64_t cnt = (int64_t)c.P * c.et_cap[t];
+    HPS_COUNT_LAUNCH();
+    gen_exact_kernel<<<(unsigned)((cnt + 255) / 256), 256>>>(c, in->d_te, in->d_gex, t, cnt);
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaDeviceSynchronize());
@@ -1184,7 +1216,7 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
     cls[e] = it->second;
   }
   CUDA_TRY(cudaMemcpy(in->d_cls, cls.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
-  in->tb = DeviceTables{in->d_stages, in->d_stage0, in->d_te, in->d_cls};
+  in->tb = DeviceTables{in->d_stages, in->d_stage0, in->d_te, in->d_cls, in->d_gex};
   *out = in;
   return HPS_OK;
 }
@@ -1195,6 +1227,7 @@ int hps_instance_destroy(HpsInstance* in) {
   cudaFree(in->d_stage0);
   cudaFree(in->d_te);
   cudaFree(in->d_cls);
+  cudaFree(in->d_gex);
   delete in;
   return HPS_OK;
 }

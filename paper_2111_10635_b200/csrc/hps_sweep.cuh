@@ -14,41 +14,73 @@
 //    exactly and the remaining bisection steps are comparisons mid >= tau*.
 //  * _best_candidate (ls/provisioner.py:262-314): candidates round-robin over lanes; counts are
 //    CERTIFIED arithmetic counts (reciprocal + rigorous error bound, count_cert) with the exact
-//    table search as fallback; a warm start plus a rigorous two-stage lower bound skips the
-//    candidates that cannot reach the minimum or its 1e-15 tie window; evaluated candidates use
-//    the reference's exact sequential per_second sum and its two cost divisions.
+//    table search as fallback; a warm start plus a rigorous lower bound (E >= tau at a certified
+//    breakpoint, per-round exact counts at the round's largest tau, FP32 bounds of the top
+//    stage) skips the candidates that cannot reach the minimum or its 1e-15 tie window;
+//    evaluated candidates use the reference's exact sequential per_second sum and its two cost
+//    divisions.
 #pragma once
 #include "hps_eval.cuh"
 
 namespace hps {
 
 #ifndef HPS_TOP
-#define HPS_TOP 2
+#define HPS_TOP 1
 #endif
-constexpr int kTop = HPS_TOP;   // unpinned stages bounded individually by cost_bound
+#ifndef HPS_ROUNDB
+#define HPS_ROUNDB 0   // 1: per-round exact counts at the round's largest candidate in the bound (measured slower)
+#endif
+constexpr int kTop = HPS_TOP;   // unpinned stages bounded per candidate (count_lb32)
 
 template <int MAXS>
 struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase (broadcast reads)
   double pr[MAXS];   // price per second of stage r's type
   double etp[MAXS];  // exact et at the pinned count (kmin == kmax), else unused
-  double pmin_rest;  // sum over non-top stages of price * kmin, rounded down by 1e-13
-  double ep_max;     // max over pinned stages of their exact et
-  int32_t top[kTop]; // unpinned stages with the largest price-weighted count span (-1: none)
+  float fpr[MAXS];   // pr as FP32 (bounds only)
+  int32_t kmi[MAXS]; // count at tau_hi (= kmin)
+  int32_t kma[MAXS]; // count at tau_lo (= kmax)
+  int32_t kr[MAXS];  // exact counts at the current round's largest candidate (bounds only)
+  int32_t top[kTop > 0 ? kTop : 1]; // unpinned stages with the largest price-weighted count span (-1: none)
   int32_t dom[MAXS]; // side_dominance over [tau_lo, tau_hi]: 1 oct, 2 odt, 0 both
+  int8_t lead[MAXS]; // class leader of stage r (stages of one class have identical counts)
+  int32_t gex[MAXS]; // leader r: count_r(et_r(m)) == m for m <= gex[r] (tb.gex), else 0
   double q[64];      // survivors of the lower-bound filter, evaluated 32 at a time
+  int32_t qg[64];    // their generator: (leader << 16) | m, or -1 (tau_lo / tau_hi)
 };
 
-// exact count at tau in [tau_lo, tau_hi] (count in [kmin, kmax]): certified (one side when it
-// provably dominates), table fallback
+// Exact count(tau) of unpinned stage r for tau in [tau_lo, tau_hi] (count in [kmin, kmax]) and
+// et at that count, from the threshold table: an FP32 estimate k is confirmed by
+// theta(k) <= tau < theta(k - 1) (two loads, one of which also carries et(k)); otherwise the
+// exact galloping table search from k decides. The estimate never affects the result.
 template <int MAXS>
-__device__ __forceinline__ int count_fast(double bo, const WarpSmem<MAXS>& w, int r, double tau,
-                                          int dom) {
+__device__ __forceinline__ int count_tab_est(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r,
+                                             double tau, double& et) {
   const StageEntry& s = w.st[r];
-  const int k = (dom == 1)   ? count_cert1(s.alpha, s.oma, s.rwo, tau, bo)
-                : (dom == 2) ? count_cert1(s.beta, s.omb, s.rwd, tau, bo)
-                             : count_cert(s, tau, bo);
-  if (k > 0) return k;
-  return count_tab(w.row[r], tau, (int)w.kmin[r], (int)w.kmax[r], est_count(w.st[r], tau));
+  const int dom = sw.dom[r];
+  const float tf = (float)tau;
+  float q = 1.0f;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    if (dom == 2 - side) continue;
+    const float rb = side ? s.f_rbd : s.f_rbo;
+    const float frac = side ? s.f_beta : s.f_alpha;
+    if (rb == 0.0f || frac == 0.0f) continue;
+    const float h = tf * rb - (side ? s.f_omb : s.f_oma);
+    q = (h > 0.0f) ? fmaxf(q, frac * rcp_approx_f32(h)) : 3.0e38f;
+  }
+  const int lo = sw.kmi[r], hi = sw.kma[r];
+  int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
+  k = min(max(k, lo), hi);
+  const TEPair* row = w.row[r];
+  const TEPair pk = row[k - 1];   // {et(k), theta(k - 1)}
+  const double thk = row[k].th;   // theta(k)
+  if (thk <= tau && tau < pk.th) {
+    et = pk.et;
+    return k;
+  }
+  k = count_tab(row, tau, lo, hi, k);
+  et = row[k - 1].et;
+  return k;
 }
 
 struct CostScalars {  // the four job constants the cost needs (no parameter-struct copies)
@@ -57,10 +89,13 @@ struct CostScalars {  // the four job constants the cost needs (no parameter-str
 
 // exact cost of candidate tau (numpy column of _best_candidate, ls/provisioner.py:286-308);
 // one out-of-line copy shared by every call site
+// gen = (g << 16) | m when tau = et_g(m) and tb.gex certifies count_g(tau) == m: every stage of
+// g's class then has count m and et == tau exactly (the breakpoint value itself).
 template <int MAXS>
 __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<MAXS>& w,
-                                          const SweepSmem<MAXS>& sw, int S, double tau) {
+                                          const SweepSmem<MAXS>& sw, int S, double tau, int gen) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const int g = (gen >= 0) ? (gen >> 16) : -1, gm = gen & 0xffff;
   double P = 0.0, E = 0.0;
   for (int r = 0; r < S; r++) {
     double et;
@@ -68,9 +103,11 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<M
     if (w.kmax[r] == w.kmin[r]) {
       k = (int)w.kmin[r];
       et = sw.etp[r];
+    } else if (sw.lead[r] == g) {
+      k = gm;
+      et = tau;
     } else {
-      k = count_fast<MAXS>(cs.bo, w, r, tau, sw.dom[r]);
-      et = w.row[r][k - 1].et;
+      k = count_tab_est<MAXS>(w, sw, r, tau, et);
     }
     E = (r == 0) ? et : fmax(E, et);
     const double term = sw.pr[r] * (double)k;
@@ -81,47 +118,59 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<M
   return cs.work / thr * P;
 }
 
-// rigorous lower bound from FP32 one-sided count bounds of the two top stages and count(tau_hi)
-// for the others: P >= sum price k_lo, E >= max(pinned et, et(k_hi) of the top stages).
-// Everything FP32 carries a 1e-5 relative slack, so the bound never exceeds the exact cost.
-template <int MAXS>
-__device__ __forceinline__ double cost_bound(const CostScalars cs, const WarpSmem<MAXS>& w,
-                                             const SweepSmem<MAXS>& sw, double tau) {
-  const float tf = (float)tau;
-  float P = (float)sw.pmin_rest, E = (float)sw.ep_max;
+// FP32 lower bound on count(tau) of an unpinned stage (pruning only). Every FP32 input and
+// operation carries a relative error of a few 2^-24; with kappa = B/h the headroom's relative
+// error is <= 3e-7 kappa + 6e-8, so q~ = frac/h~ is within q (1 +- e0), e0 = 4e-7 (kappa + 2).
+// lo = q~ (1 - e0 - 1e-6) is then <= q - 1e-9 whenever lo >= 1 (q >= 1e-3), and iceil is
+// monotone, so ceil(lo) <= ceil(q - 1e-9) = count. dom (side_dominance) restricts it to the
+// deciding side; a side with too much cancellation is skipped (1 is always a lower bound).
+__device__ __forceinline__ int count_lb32(const StageEntry& s, float tau, int dom) {
+  float lo = 1.0f;
 #pragma unroll
-  for (int q = 0; q < kTop; q++) {
-    const int r = sw.top[q];
-    if (r < 0) continue;
-    int kl, ku;
-    count_bounds32(w.st[r], tf, sw.dom[r], kl, ku);
-    const int lo = (int)w.kmin[r], hi = (int)w.kmax[r];
-    kl = max(kl, lo);
-    P += (float)sw.pr[r] * (float)kl;
-    if (ku > 0) {
-      const StageEntry& st = w.st[r];
-      const float k = (float)min(ku, hi);
-      const float rk = rcp_approx_f32(k);
-      E = fmaxf(E, fmaxf(st.f_coct * (st.f_oma + st.f_alpha * rk), st.f_codt * (st.f_omb + st.f_beta * rk)));
-    }
+  for (int side = 0; side < 2; side++) {
+    if (dom == 2 - side) continue;   // dom 1 skips side 1, dom 2 skips side 0
+    const float rb = side ? s.f_rbd : s.f_rbo;
+    const float frac = side ? s.f_beta : s.f_alpha;
+    if (rb == 0.0f || frac == 0.0f) continue;
+    const float omf = side ? s.f_omb : s.f_oma;
+    const float B = tau * rb;
+    const float h = B - omf;
+    if (!(h > 1e-3f * B)) continue;
+    const float rh = rcp_approx_f32(h);
+    const float e = 4e-7f * (B * rh + 2.0f) + 1e-6f;
+    lo = fmaxf(lo, (frac * rh) * (1.0f - e));
   }
-  return (double)((float)(cs.work / cs.batch) * E * P) * (1.0 - 1e-5);
+  return (int)ceilf(lo);
 }
 
+// candidate i: tau_lo, tau_hi, then the breakpoints et_sp(m) of the class leaders; gen as in
+// cost_exact (-1 unless the leader's breakpoints are certified)
 template <int MAXS>
-__device__ __forceinline__ double cand_tau(const WarpSmem<MAXS>& w, int i, int& sp, double tau_lo,
-                                           double tau_hi) {
+__device__ __forceinline__ double cand_tau(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int i,
+                                           int& sp, double tau_lo, double tau_hi, int& gen) {
+  gen = -1;
   if (i < 2) return (i == 0) ? tau_lo : tau_hi;
   const int j = i - 2;
   while (w.pre[sp + 1] <= j) sp++;
   const int m = (int)w.kmin[sp] + (j - w.pre[sp]);
+  if (m <= sw.gex[sp]) gen = (sp << 16) | m;
   return w.row[sp][m - 1].et;
 }
 
-// _best_candidate: round-robin candidates over lanes. A warm-start pass evaluates every 8th
-// round exactly; the remaining candidates are evaluated exactly only when a rigorous lower bound
-// (two top stages exact) does not exceed the best cost so far + 1e-15. A skipped candidate
-// therefore costs more than the final minimum + 1e-15: it is neither the minimum nor a tie.
+// _best_candidate: round-robin candidates over lanes. A warm-start round evaluates 32 candidates
+// spread over the candidate range exactly; every other candidate is evaluated exactly only when a
+// rigorous lower bound on its cost does not exceed the best cost so far + 1e-15. A skipped
+// candidate therefore costs more than the final minimum + 1e-15: neither the minimum nor a tie.
+//
+// The bound of a certified breakpoint tau = et_g(m) (count_g(tau) == m, tb.gex): cost =
+// (work/batch) E P with E >= et_g(m) = tau and P = sum_r pr_r count_r(tau), where
+//   * count_g(tau) = m;
+//   * count_r(tau) >= count_r(tau_max) for every r, tau_max = the round's largest candidate
+//     (counts are non-increasing in tau): exact counts at tau_max are computed once per round,
+//     one stage per lane, and the warp sums them;
+//   * the top stage(s) also get a per-candidate FP32 lower bound (count_lb32).
+// All FP32 arithmetic of the bound is covered by a 1e-5 relative slack. tau_lo, tau_hi and
+// uncertified breakpoints are always evaluated.
 template <int MAXS>
 __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTables& tb,
                                         const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
@@ -129,19 +178,26 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   for (int r = lane; r < S; r += 32) {
+    const bool pinned = (w.kmax[r] == w.kmin[r]);
     sw.pr[r] = c.price_s[w.st[r].type];
-    sw.etp[r] = (w.kmax[r] == w.kmin[r]) ? w.row[r][(int)w.kmin[r] - 1].et : 0.0;
-    sw.dom[r] = (w.kmax[r] == w.kmin[r]) ? 0 : side_dominance(w.st[r], tau_lo, tau_hi, c.bo);
+    sw.fpr[r] = (float)sw.pr[r];
+    sw.kmi[r] = (int)w.kmin[r];
+    sw.kma[r] = (int)w.kmax[r];
+    sw.etp[r] = pinned ? w.row[r][(int)w.kmin[r] - 1].et : 0.0;
+    sw.dom[r] = pinned ? 0 : side_dominance(w.st[r], tau_lo, tau_hi, c.bo);
+    int ld = 0;  // first stage of r's class
+    while (w.cls[ld] != w.cls[r]) ld++;
+    sw.lead[r] = (int8_t)ld;
+    sw.gex[r] = (ld == r && !pinned) ? __ldg(tb.gex + w.ent[r]) : 0;
   }
   __syncwarp();
   if (lane == 0) {
-    int t[kTop];
-    double v[kTop];
+    int t[kTop > 0 ? kTop : 1];
+    double v[kTop > 0 ? kTop : 1];
 #pragma unroll
     for (int q = 0; q < kTop; q++) { t[q] = -1; v[q] = -1.0; }
-    double ep = 0.0;
     for (int r = 0; r < S; r++) {
-      if (w.kmax[r] == w.kmin[r]) { ep = fmax(ep, sw.etp[r]); continue; }
+      if (w.kmax[r] == w.kmin[r]) continue;
       double vv = sw.pr[r] * (w.kmax[r] - w.kmin[r]);
       int tt = r;
 #pragma unroll
@@ -152,17 +208,8 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
         }
       }
     }
-    double pm = 0.0;
-    for (int r = 0; r < S; r++) {
-      bool in_top = false;
-#pragma unroll
-      for (int q = 0; q < kTop; q++) in_top |= (t[q] == r);
-      if (!in_top) pm += sw.pr[r] * w.kmin[r];
-    }
 #pragma unroll
     for (int q = 0; q < kTop; q++) sw.top[q] = t[q];
-    sw.pmin_rest = pm * (1.0 - 1e-13);
-    sw.ep_max = ep;
     HPS_STAT(ST_NCAND, n_cand);
     HPS_STAT(ST_PLANS_FAST, 1);
     HPS_STAT(ST_STAGES, S);
@@ -175,13 +222,27 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   int sp = 0;
   {  // warm start: one round of 32 candidates spread evenly over the candidate range
     const int i = (int)(((long long)lane * n_cand) >> 5);
-    const double tau = cand_tau<MAXS>(w, i, sp, tau_lo, tau_hi);
+    int gen;
+    const double tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
     if (tau >= tau_lo && tau <= tau_hi) {
       HPS_STAT(ST_CANDS, 1);
-      buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau), tau);
+      buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau, gen), tau);
     }
   }
   double ub = warp_min(buf.mn);
+  const float fC = (float)(c.work / c.batch);
+#if !HPS_ROUNDB
+  float pl0 = 0.0f;  // counts at tau_hi
+  for (int r = lane; r < S; r += 32) {
+    sw.kr[r] = sw.kmi[r];
+    pl0 += sw.fpr[r] * (float)sw.kmi[r];
+  }
+  for (int o = 16; o; o >>= 1) pl0 += __shfl_xor_sync(0xffffffffu, pl0, o);
+  __syncwarp();
+#endif
+  int top[kTop > 0 ? kTop : 1];
+#pragma unroll
+  for (int q = 0; q < kTop; q++) top[q] = sw.top[q];
   // every candidate: lower-bound filter; survivors are compacted into sw.q and evaluated
   // densely (a warp only saves work when all 32 lanes skip, so skipping must be compacted).
   // A warm-start candidate may pass again; re-inserting it is harmless (same cost and tau).
@@ -190,20 +251,52 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   const unsigned lt = (1u << lane) - 1u;
   for (int jr = 0; jr < rounds; jr++) {
     const int i = jr * 32 + lane;
-    bool keep = false;
     double tau = 0.0;
+    int gen = -1;
+    bool inr = false;
     if (i < n_cand) {
-      tau = cand_tau<MAXS>(w, i, sp, tau_lo, tau_hi);
-      keep = tau >= tau_lo && tau <= tau_hi && !(cost_bound<MAXS>(cs, w, sw, tau) > ub + 1e-15);
+      tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
+      inr = tau >= tau_lo && tau <= tau_hi;
+    }
+    const double tmax = warp_max(inr ? tau : -inf);
+    if (!(tmax > -inf)) continue;  // warp-uniform
+#if HPS_ROUNDB
+    float pl = 0.0f;
+    for (int r = lane; r < S; r += 32) {
+      int k = sw.kmi[r];
+      double et_unused;
+      if (sw.kma[r] != k) k = count_tab_est<MAXS>(w, sw, r, tmax, et_unused);
+      sw.kr[r] = k;
+      pl += sw.fpr[r] * (float)k;
+    }
+    for (int o = 16; o; o >>= 1) pl += __shfl_xor_sync(0xffffffffu, pl, o);
+    __syncwarp();
+#else
+    const float pl = pl0;
+#endif
+    bool keep = inr;
+    if (inr && gen >= 0) {
+      const int g = gen >> 16, m = gen & 0xffff;
+      const float tf = (float)tau;
+      float P = pl + sw.fpr[g] * (float)(m - sw.kr[g]);
+#pragma unroll
+      for (int q = 0; q < kTop; q++) {
+        const int r = top[q];
+        if (r < 0 || r == g) continue;
+        const int d = count_lb32(w.st[r], tf, sw.dom[r]) - sw.kr[r];
+        if (d > 0) P += sw.fpr[r] * (float)d;
+      }
+      keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > ub + 1e-15);
     }
     const unsigned mk = __ballot_sync(0xffffffffu, keep);
-    if (keep) sw.q[qn + __popc(mk & lt)] = tau;
+    if (keep) { sw.q[qn + __popc(mk & lt)] = tau; sw.qg[qn + __popc(mk & lt)] = gen; }
     qn += __popc(mk);
     __syncwarp();
     if (qn >= 32) {
       const double t = sw.q[qn - 32 + lane];
+      const int tg = sw.qg[qn - 32 + lane];
       HPS_STAT(ST_CANDS, 1);
-      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t), t);
+      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t, tg), t);
       qn -= 32;
       ub = fmin(ub, warp_min(buf.mn));
       __syncwarp();
@@ -213,32 +306,21 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     if (lane < qn) {
       const double t = sw.q[lane];
       HPS_STAT(ST_CANDS, 1);
-      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t), t);
+      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t, sw.qg[lane]), t);
     }
   }
   const double mf = warp_min(buf.mn);
   if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
   const double lim = mf + 1e-15;
-#ifdef HPS_STATS
-  {  // diagnostics: survivors the filter would keep with the final minimum as its bound
-    int sp2 = 0, ideal = 0, unp = 0;
-    for (int i = lane; i < n_cand; i += 32) {
-      const double tau = cand_tau<MAXS>(w, i, sp2, tau_lo, tau_hi);
-      if (tau >= tau_lo && tau <= tau_hi && !(cost_bound<MAXS>(cs, w, sw, tau) > lim)) ideal++;
-    }
-    for (int r = lane; r < S; r += 32) unp += (w.kmax[r] != w.kmin[r]);
-    HPS_STAT(ST_CHUNKS, ideal);
-    HPS_STAT(ST_UNPINNED, unp);
-  }
-#endif
   double bt;
   if (__any_sync(0xffffffffu, buf.overflow)) {  // rare: exact second pass with the final limit
     bt = -inf;
     sp = 0;
     for (int i = lane; i < n_cand; i += 32) {
-      const double tau = cand_tau<MAXS>(w, i, sp, tau_lo, tau_hi);
+      int gen;
+      const double tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
       if (!(tau >= tau_lo && tau <= tau_hi) || !(tau > bt)) continue;
-      if (!(cost_bound<MAXS>(cs, w, sw, tau) > lim) && cost_exact<MAXS>(cs, w, sw, S, tau) <= lim) bt = tau;
+      if (cost_exact<MAXS>(cs, w, sw, S, tau, gen) <= lim) bt = tau;
     }
   } else {
     bt = buf.best_tau(lim);

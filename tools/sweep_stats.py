@@ -7,7 +7,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-NAMES = ["plans", "ideal_survivors", "unused", "cands_eval", "probes_exact", "probes_closed", "cert",
+NAMES = ["plans", "ideal_survivors", "gen_certified", "cands_eval", "probes_exact", "probes_closed", "cert",
          "cert_fail", "tab", "pending", "stages", "unpinned", "ncand", "plans_fast", "cyc_stages_bisect", "cyc_candidates",
          "cyc_final", "cyc_pass1", "cyc_pass2"]
 
@@ -17,8 +17,9 @@ def main():
     ap.add_argument("--instance", default="cfg3")
     ap.add_argument("--begin", type=int, default=3 ** 16 // 2)
     ap.add_argument("--count", type=int, default=1 << 16)
+    ap.add_argument("--lib", default="libhps_stats.so")
     a = ap.parse_args()
-    os.environ["HPS_LIBRARY"] = str(ROOT / "paper_2111_10635_b200" / "libhps_stats.so")
+    os.environ["HPS_LIBRARY"] = str(ROOT / "paper_2111_10635_b200" / a.lib)
     import torch
     from paper_2111_10635_b200 import _abi, load_fixture
     from paper_2111_10635_b200.instance import DeviceInstance
