@@ -21,6 +21,10 @@
 
 namespace hps {
 
+#ifndef HPS_BISECT_PROBES
+#define HPS_BISECT_PROBES 0   // 1: the probing bisection (bisect_fast) instead of bisect_direct
+#endif
+
 constexpr int kTieBuf = 4;
 constexpr uint8_t kStPending = 0xFE;  // internal: needs the block-per-plan slow path
 
@@ -329,6 +333,199 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
 }
 
 
+// Exact count(tau) of a stage known to lie in [lo, hi] (hi <= table cap): FP32 seed, confirmed by
+// theta(k) <= tau < theta(k - 1) or corrected by the galloping table search.
+__device__ __forceinline__ int count_seeded(const StageEntry& s, const TEPair* row, double tau, int lo, int hi) {
+  const float tf = (float)tau;
+  float q = 1.0f;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const float rb = side ? s.f_rbd : s.f_rbo;
+    const float frac = side ? s.f_beta : s.f_alpha;
+    if (rb == 0.0f || frac == 0.0f) continue;
+    const float h = tf * rb - (side ? s.f_omb : s.f_oma);
+    q = (h > 0.0f) ? fmaxf(q, frac * rcp_approx_f32(h)) : 3.0e38f;
+  }
+  int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
+  k = min(max(k, lo), hi);
+  const double2 pk = __ldg(reinterpret_cast<const double2*>(row + (k - 1)));  // {et(k), theta(k-1)}
+  const double thk = __ldg(&row[k].th);
+  if (thk <= tau && tau < pk.y) return k;
+  return count_tab(row, tau, lo, hi, k);
+}
+
+// FP32 continuous count q(tau) = max(1, frac / (tau rb - (1 - frac))) of both sides and dq/dtau
+// (seed arithmetic only)
+__device__ __forceinline__ float q_cont(const StageEntry& s, float tau, float& dq) {
+  float q = 1.0f;
+  dq = 0.0f;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const float rb = side ? s.f_rbd : s.f_rbo;
+    const float frac = side ? s.f_beta : s.f_alpha;
+    if (rb == 0.0f || frac == 0.0f) continue;
+    const float h = tau * rb - (side ? s.f_omb : s.f_oma);
+    const float v = (h > 0.0f) ? frac / h : 3.0e38f;
+    if (v > q) { q = v; dq = (h > 0.0f) ? -v * rb / h : -3.0e38f; }
+  }
+  return q;
+}
+
+// Quota bisection (ls/provisioner.py:430-437) by its switch point. quota_ok(tau) holds iff for
+// every type t the sum of its stages' counts is <= Q_t, and counts are non-increasing
+// right-continuous step functions (count(tau) <= k <=> tau >= theta(k)), so quota_ok(tau) <=>
+// tau >= tau* = max_t tau*_t. Per type: tau*_t >= L_t = max_r theta_r(Q_t) (below it one stage
+// alone exceeds the quota); an FP32 Newton solve of sum_r q_r(tau) = Q_t - n/2 seeds tau_e in
+// [L_t, tau_hi]; the exact counts at tau_e (sum S_e) then select tau*_t exactly from the
+// thresholds next to tau_e: if S_e <= Q_t it is the (Q_t - S_e + 1)-th largest threshold below
+// (count increments), else the (S_e - Q_t)-th smallest above (decrements), never below L_t.
+// With tau* exact, the reference's 60 halvings are replayed as comparisons mid >= tau*, and the
+// counts at the final b (= tau_lo) are read from the tables. Mids in (serial, tau_hi) never
+// raise in _floor_count except where counts exceed every quota (mid < L_t), where quota_ok is
+// false either way.
+static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, const StageEntry* st,
+                                                    const TEPair* const* rows, int S, double a, double b,
+                                                    const double kb_in[2], int kb_out[2]) {
+  const int lane = threadIdx.x & 31;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  int ty[2], kb[2];
+  const TEPair* row[2];
+#pragma unroll
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    ty[slot] = (s < S) ? st[s].type : -1;
+    kb[slot] = (s < S) ? (int)kb_in[slot] : 0;
+    row[slot] = (s < S) ? rows[s] : nullptr;
+  }
+  const unsigned present =
+      __reduce_or_sync(0xffffffffu, (ty[0] >= 0 ? 1u << ty[0] : 0u) | (ty[1] >= 0 ? 1u << ty[1] : 0u));
+  double tstar = -inf;
+  unsigned rem = present;
+  while (rem) {
+    const int t = __ffs(rem) - 1;
+    rem &= rem - 1;
+    const int Q = (int)c.quota[t];
+    const bool mb[2] = {ty[0] == t, ty[1] == t};
+    double lt = -inf;
+#pragma unroll
+    for (int slot = 0; slot < 2; slot++)
+      if (mb[slot]) lt = fmax(lt, __ldg(&row[slot][Q].th));
+    lt = warp_max(lt);
+    // exact counts at L_t (each <= Q there): when their sum is within the quota, tau*_t = L_t
+    int cnt[2] = {0, 0};
+#pragma unroll
+    for (int slot = 0; slot < 2; slot++)
+      if (mb[slot]) cnt[slot] = count_seeded(st[lane + 32 * slot], row[slot], lt, kb[slot], Q);
+    const int sl = (int)__reduce_add_sync(0xffffffffu, (unsigned)(cnt[0] + cnt[1]));
+    if (sl <= Q) {
+      tstar = fmax(tstar, lt);
+      continue;
+    }
+    // ---- FP32 seed of the root of sum_r q_r(tau) = Q_t - n/2 in (L_t, tau_hi]: Newton on
+    // 1/F - 1/target from L_t (exact in one step for a single hyperbola c/(tau - p)) ----
+    const int n = (int)__reduce_add_sync(0xffffffffu, (unsigned)mb[0] + (unsigned)mb[1]);
+    const float target = (float)Q - 0.5f * (float)n;
+    const float flo = (float)lt, fhi = (float)b;
+    float x = flo;
+    for (int itn = 0; itn < 12; itn++) {
+      if (lane == 0) HPS_STAT(ST_CERT, 1);
+      float F = 0.0f, dF = 0.0f;
+#pragma unroll
+      for (int slot = 0; slot < 2; slot++)
+        if (mb[slot]) {
+          float d;
+          F += q_cont(st[lane + 32 * slot], x, d);
+          dF += d;
+        }
+      for (int o = 16; o; o >>= 1) {
+        F += __shfl_xor_sync(0xffffffffu, F, o);
+        dF += __shfl_xor_sync(0xffffffffu, dF, o);
+      }
+      if (fabsf(F - target) <= 0.25f || !(dF < 0.0f) || !(F < 3.0e37f)) break;
+      float nx = x + F * (1.0f - F / target) / dF;
+      nx = fminf(fmaxf(nx, flo), fhi);
+      const bool done = fabsf(nx - x) <= 1e-7f * x;
+      x = nx;
+      if (done) break;
+    }
+    double te = fmin(fmax((double)x, lt), b);
+    // ---- exact counts at te and exact selection of tau*_t ----
+#pragma unroll
+    for (int slot = 0; slot < 2; slot++)
+      if (mb[slot]) cnt[slot] = count_seeded(st[lane + 32 * slot], row[slot], te, kb[slot], Q);
+    const int se = (int)__reduce_add_sync(0xffffffffu, (unsigned)(cnt[0] + cnt[1]));
+    double tt;
+    if (se <= Q) {
+      // descending thresholds below te: theta_r(cnt) (count cnt -> cnt + 1 below it); only
+      // values >= L_t matter (below L_t the type is over its quota regardless)
+      double nx[2];
+#pragma unroll
+      for (int slot = 0; slot < 2; slot++) {
+        nx[slot] = -inf;
+        if (mb[slot] && cnt[slot] < Q) {
+          const double v = __ldg(&row[slot][cnt[slot]].th);
+          if (v >= lt) nx[slot] = v;
+        }
+      }
+      int d = Q - se + 1;
+      if (d > 48) return __longlong_as_double(0x7ff8000000000000LL);  // poor seed: caller falls back
+      tt = lt;
+      for (;;) {
+        const double mine = fmax(nx[0], nx[1]);
+        const double e = warp_max(mine);
+        if (lane == 0) HPS_STAT(ST_PROBES_EXACT, 1);
+        if (!(e > -inf)) { tt = lt; break; }
+        if (--d == 0) { tt = fmax(e, lt); break; }
+        const unsigned own = __ballot_sync(0xffffffffu, mine == e);
+        if (lane == __ffs(own) - 1) {
+          const int sl = (nx[0] == e) ? 0 : 1;
+          const int k = ++cnt[sl];
+          double v = -inf;
+          if (k < Q) {
+            v = __ldg(&row[sl][k].th);
+            if (!(v >= lt)) v = -inf;
+          }
+          nx[sl] = v;
+        }
+      }
+    } else {
+      // ascending thresholds above te: theta_r(cnt - 1) (count cnt -> cnt - 1 from it on), down to
+      // the count at tau_hi
+      double nx[2];
+#pragma unroll
+      for (int slot = 0; slot < 2; slot++)
+        nx[slot] = (mb[slot] && cnt[slot] > kb[slot]) ? __ldg(&row[slot][cnt[slot] - 1].th) : inf;
+      int d = se - Q;
+      if (d > 48) return __longlong_as_double(0x7ff8000000000000LL);
+      tt = b;
+      for (;;) {
+        const double mine = fmin(nx[0], nx[1]);
+        const double e = warp_min(mine);
+        if (lane == 0) HPS_STAT(ST_CERT_FAIL, 1);
+        if (!(e < inf)) { tt = b; break; }  // (cannot happen: quota_ok(tau_hi) holds)
+        if (--d == 0) { tt = e; break; }
+        const unsigned own = __ballot_sync(0xffffffffu, mine == e);
+        if (lane == __ffs(own) - 1) {
+          const int sl = (nx[0] == e) ? 0 : 1;
+          const int k = --cnt[sl];
+          nx[sl] = (k > kb[sl]) ? __ldg(&row[sl][k - 1].th) : inf;
+        }
+      }
+    }
+    tstar = fmax(tstar, tt);
+  }
+  if (lane == 0) HPS_STAT(ST_PROBES_CLOSED, 60);
+  for (int it = 0; it < 60; it++) {
+    const double mid = (a + b) / 2.0;
+    if (mid >= tstar) b = mid; else a = mid;
+  }
+#pragma unroll
+  for (int slot = 0; slot < 2; slot++)
+    kb_out[slot] = (ty[slot] >= 0) ? count_seeded(st[lane + 32 * slot], row[slot], b, kb[slot], (int)c.quota[ty[slot]])
+                                   : kb[slot];
+  return b;
+}
+
 // Evaluate one candidate tau: numpy _best_candidate column (ls/provisioner.py:286-308).
 // Returns +inf when the column is not ok (throughput <= limit).
 template <int MAXS, bool CERT = false>
@@ -476,7 +673,16 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
   double a = ser, b = tau_hi;
   if (FAST) {
     int kl[2];
+#if HPS_BISECT_PROBES
     b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
+#else
+    const double bd = bisect_direct(c, w.st, w.row, S, a, b, kb, kl);
+    if (bd == bd) b = bd;
+    else {  // (rare) seed too far off
+      if ((threadIdx.x & 31) == 0) HPS_STAT(ST_UNPINNED, 1);
+      b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
+    }
+#endif
     kb[0] = (double)kl[0];
     kb[1] = (double)kl[1];
   } else {

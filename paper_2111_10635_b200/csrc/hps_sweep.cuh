@@ -40,6 +40,7 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   int32_t kmi[MAXS]; // count at tau_hi (= kmin)
   int32_t kma[MAXS]; // count at tau_lo (= kmax)
   int32_t kr[MAXS];  // exact counts at the current round's largest candidate (bounds only)
+
   int32_t top[kTop > 0 ? kTop : 1]; // unpinned stages with the largest price-weighted count span (-1: none)
   int32_t dom[MAXS]; // side_dominance over [tau_lo, tau_hi]: 1 oct, 2 odt, 0 both
   int8_t lead[MAXS]; // class leader of stage r (stages of one class have identical counts)
@@ -48,16 +49,12 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   int32_t qg[64];    // their generator: (leader << 16) | m, or -1 (tau_lo / tau_hi)
 };
 
-// Exact count(tau) of unpinned stage r for tau in [tau_lo, tau_hi] (count in [kmin, kmax]) and
-// et at that count, from the threshold table: an FP32 estimate k is confirmed by
-// theta(k) <= tau < theta(k - 1) (two loads, one of which also carries et(k)); otherwise the
-// exact galloping table search from k decides. The estimate never affects the result.
+// FP32 estimate of count(tau) of unpinned stage r, clamped to [kmin, kmax]. Only a seed: the
+// threshold table confirms or corrects it (count_verify), so it never affects a result.
 template <int MAXS>
-__device__ __forceinline__ int count_tab_est(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r,
-                                             double tau, double& et) {
+__device__ __forceinline__ int count_est(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r, float tf) {
   const StageEntry& s = w.st[r];
   const int dom = sw.dom[r];
-  const float tf = (float)tau;
   float q = 1.0f;
 #pragma unroll
   for (int side = 0; side < 2; side++) {
@@ -69,17 +66,30 @@ __device__ __forceinline__ int count_tab_est(const WarpSmem<MAXS>& w, const Swee
     q = (h > 0.0f) ? fmaxf(q, frac * rcp_approx_f32(h)) : 3.0e38f;
   }
   const int lo = sw.kmi[r], hi = sw.kma[r];
-  int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
-  k = min(max(k, lo), hi);
-  const TEPair* row = w.row[r];
-  const TEPair pk = row[k - 1];   // {et(k), theta(k - 1)}
-  const double thk = row[k].th;   // theta(k)
-  if (thk <= tau && tau < pk.th) {
-    et = pk.et;
+  const int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
+  return min(max(k, lo), hi);
+}
+
+// read-only table loads: {et(k), theta(k - 1)} in one 16-byte load, theta(k) separately
+__device__ __forceinline__ double2 te_pair(const TEPair* row, int k) {
+  return __ldg(reinterpret_cast<const double2*>(row + (k - 1)));
+}
+__device__ __forceinline__ double te_theta(const TEPair* row, int k) { return __ldg(&row[k].th); }
+
+// Exact count(tau) for tau in [tau_lo, tau_hi] (count in [kmin, kmax]) given the seed k and the
+// loads pk = {et(k), theta(k - 1)}, thk = theta(k): k is the count iff theta(k) <= tau <
+// theta(k - 1) (count(tau) = min{m : theta(m) <= tau}); otherwise the exact galloping table search
+// from k decides. Returns the count and et at it.
+template <int MAXS>
+__device__ __forceinline__ int count_verify(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r,
+                                            double tau, int k, double2 pk, double thk, double& et) {
+  if (thk <= tau && tau < pk.y) {
+    et = pk.x;
     return k;
   }
-  k = count_tab(row, tau, lo, hi, k);
-  et = row[k - 1].et;
+  const TEPair* row = w.row[r];
+  k = count_tab(row, tau, sw.kmi[r], sw.kma[r], k);
+  et = __ldg(&row[k - 1].et);
   return k;
 }
 
@@ -88,7 +98,7 @@ struct CostScalars {  // the four job constants the cost needs (no parameter-str
 };
 
 // exact cost of candidate tau (numpy column of _best_candidate, ls/provisioner.py:286-308);
-// one out-of-line copy shared by every call site
+// one out-of-line copy shared by every call site.
 // gen = (g << 16) | m when tau = et_g(m) and tb.gex certifies count_g(tau) == m: every stage of
 // g's class then has count m and et == tau exactly (the breakpoint value itself).
 template <int MAXS>
@@ -96,18 +106,21 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<M
                                           const SweepSmem<MAXS>& sw, int S, double tau, int gen) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   const int g = (gen >= 0) ? (gen >> 16) : -1, gm = gen & 0xffff;
+  const float tf = (float)tau;
   double P = 0.0, E = 0.0;
   for (int r = 0; r < S; r++) {
     double et;
     int k;
-    if (w.kmax[r] == w.kmin[r]) {
-      k = (int)w.kmin[r];
+    if (sw.kma[r] == sw.kmi[r]) {
+      k = sw.kmi[r];
       et = sw.etp[r];
     } else if (sw.lead[r] == g) {
       k = gm;
       et = tau;
     } else {
-      k = count_tab_est<MAXS>(w, sw, r, tau, et);
+      const int k0 = count_est<MAXS>(w, sw, r, tf);
+      const TEPair* row = w.row[r];
+      k = count_verify<MAXS>(w, sw, r, tau, k0, te_pair(row, k0), te_theta(row, k0), et);
     }
     E = (r == 0) ? et : fmax(E, et);
     const double term = sw.pr[r] * (double)k;
@@ -154,7 +167,7 @@ __device__ __forceinline__ double cand_tau(const WarpSmem<MAXS>& w, const SweepS
   while (w.pre[sp + 1] <= j) sp++;
   const int m = (int)w.kmin[sp] + (j - w.pre[sp]);
   if (m <= sw.gex[sp]) gen = (sp << 16) | m;
-  return w.row[sp][m - 1].et;
+  return __ldg(&w.row[sp][m - 1].et);
 }
 
 // _best_candidate: round-robin candidates over lanes. A warm-start round evaluates 32 candidates
@@ -210,6 +223,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     }
 #pragma unroll
     for (int q = 0; q < kTop; q++) sw.top[q] = t[q];
+
     HPS_STAT(ST_NCAND, n_cand);
     HPS_STAT(ST_PLANS_FAST, 1);
     HPS_STAT(ST_STAGES, S);
@@ -265,7 +279,10 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     for (int r = lane; r < S; r += 32) {
       int k = sw.kmi[r];
       double et_unused;
-      if (sw.kma[r] != k) k = count_tab_est<MAXS>(w, sw, r, tmax, et_unused);
+      if (sw.kma[r] != k) {
+        const int k0 = count_est<MAXS>(w, sw, r, (float)tmax);
+        k = count_verify<MAXS>(w, sw, r, tmax, k0, te_pair(w.row[r], k0), te_theta(w.row[r], k0), et_unused);
+      }
       sw.kr[r] = k;
       pl += sw.fpr[r] * (float)k;
     }

@@ -8,7 +8,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 NAMES = ["plans", "ideal_survivors", "gen_certified", "cands_eval", "probes_exact", "probes_closed", "cert",
-         "cert_fail", "tab", "pending", "stages", "unpinned", "ncand", "plans_fast", "cyc_stages_bisect", "cyc_candidates",
+         "cert_fail", "tab", "pending", "stages", "bisect_fallback", "ncand", "plans_fast", "cyc_stages_bisect", "cyc_candidates",
          "cyc_final", "cyc_pass1", "cyc_pass2"]
 
 
