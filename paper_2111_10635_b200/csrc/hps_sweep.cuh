@@ -27,9 +27,6 @@ namespace hps {
 #ifndef HPS_TOP
 #define HPS_TOP 1
 #endif
-#ifndef HPS_ROUNDB
-#define HPS_ROUNDB 0   // 1: per-round exact counts at the round's largest candidate in the bound (measured slower)
-#endif
 constexpr int kTop = HPS_TOP;   // unpinned stages bounded per candidate (count_lb32)
 
 template <int MAXS>
@@ -39,7 +36,8 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   float fpr[MAXS];   // pr as FP32 (bounds only)
   int32_t kmi[MAXS]; // count at tau_hi (= kmin)
   int32_t kma[MAXS]; // count at tau_lo (= kmax)
-  int32_t kr[MAXS];  // exact counts at the current round's largest candidate (bounds only)
+  int32_t alo[MAXS], an[MAXS], blo[MAXS];  // restricted candidate ranges (cand_tau2)
+  int32_t pre2[MAXS + 1];
 
   int32_t top[kTop > 0 ? kTop : 1]; // unpinned stages with the largest price-weighted count span (-1: none)
   int32_t dom[MAXS]; // side_dominance over [tau_lo, tau_hi]: 1 oct, 2 odt, 0 both
@@ -170,20 +168,104 @@ __device__ __forceinline__ double cand_tau(const WarpSmem<MAXS>& w, const SweepS
   return __ldg(&w.row[sp][m - 1].et);
 }
 
+// candidate i of the restricted list: tau_lo, tau_hi, then per class leader sp the certified
+// breakpoints m in [alo, alo + an) (those inside the bound interval) and the uncertified ones
+// m in [blo, kmax]
+template <int MAXS>
+__device__ __forceinline__ double cand_tau2(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int i,
+                                            int& sp, double tau_lo, double tau_hi, int& gen) {
+  gen = -1;
+  if (i < 2) return (i == 0) ? tau_lo : tau_hi;
+  const int j = i - 2;
+  while (sw.pre2[sp + 1] <= j) sp++;
+  const int o = j - sw.pre2[sp];
+  int m;
+  if (o < sw.an[sp]) {
+    m = sw.alo[sp] + o;
+    gen = (sp << 16) | m;
+  } else {
+    m = sw.blo[sp] + (o - sw.an[sp]);
+  }
+  return __ldg(&w.row[sp][m - 1].et);
+}
+
+// Continuous lower bound of the cost of every certified breakpoint candidate tau:
+//   L(tau) = (work/batch) tau sum_r pr_r max(kmin_r, q_r(tau)(1 - 1e-8) - 1e-9),
+// q_r = max over sides of frac / (tau bo/work - (1 - frac)): count_r(tau) = ceil(max(1, q) - 1e-9)
+// >= both terms (the 1e-8 relative slack covers the rounding of q here and in the reference), and
+// E >= tau (certified breakpoint). Each term tau max(kmin, q(1-d) - e) is a max of convex
+// functions of tau (tau q(tau) = (frac/b)(1 + c/(b tau - c)) with c = 1 - frac), so L is convex.
+// Returns L and a subgradient dL/dtau at tau.
+template <int MAXS>
+__device__ __forceinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int S, double bo,
+                                        double C, double tau, double& L, double& dL) {
+  double P = 0.0, dP = 0.0;
+  for (int r = 0; r < S; r++) {
+    const double km = (double)sw.kmi[r];
+    double v = km * tau, dv = km;
+    if (sw.kma[r] != sw.kmi[r]) {
+      const StageEntry& s = w.st[r];
+#pragma unroll
+      for (int side = 0; side < 2; side++) {
+        const double work = side ? s.odt : s.oct;
+        const double frac = side ? s.beta : s.alpha;
+        if (work == 0.0 || frac == 0.0) continue;
+        const double cc = side ? s.omb : s.oma;
+        const double h = tau * (bo * (side ? s.rwd : s.rwo)) - cc;
+        if (!(h > 0.0)) { v = __longlong_as_double(0x7ff0000000000000LL); dv = 0.0; continue; }
+        const double q = frac * rcp_1nt(h);
+        const double vq = tau * (q * (1.0 - 1e-8) - 1e-9);
+        if (vq > v) { v = vq; dv = (1.0 - 1e-8) * (-q * q * cc / frac) - 1e-9; }
+      }
+    }
+    P += sw.pr[r] * v;
+    dP += sw.pr[r] * dv;
+  }
+  L = C * P;
+  dL = C * dP;
+}
+
+// One level of the interval search: lane j holds (t, L, dL) at grid point j of [ta, tb] (lane
+// 31 = tb). On each cell, convexity bounds L from below by max(tangent at the left end, tangent
+// at the right end); [ta, tb] shrinks to the cells whose bound does not exceed thr (ta > tb when
+// none does).
+__device__ __forceinline__ void interval_cells(double t, double L, double d, double thr, double& ta, double& tb) {
+  const int lane = threadIdx.x & 31;
+  const double t1 = __shfl_down_sync(0xffffffffu, t, 1);
+  const double L1 = __shfl_down_sync(0xffffffffu, L, 1);
+  const double d1 = __shfl_down_sync(0xffffffffu, d, 1);
+  double lb;
+  if (d >= 0.0) lb = L;
+  else if (d1 <= 0.0) lb = L1;
+  else {
+    const double x = (L1 - L + d * t - d1 * t1) / (d - d1);
+    lb = fmin(L + d * (x - t), fmin(L, L1));
+  }
+  const bool keep = (lane < 31) && !(lb > thr);   // NaN keeps
+  const unsigned mk = __ballot_sync(0xffffffffu, keep);
+  if (!mk) { ta = 1.0; tb = 0.0; return; }
+  const int f = __ffs(mk) - 1, l = 31 - __clz(mk);
+  const double nta = __shfl_sync(0xffffffffu, t, f);
+  tb = __shfl_sync(0xffffffffu, t, l + 1);
+  ta = nta;
+}
+
+template <int MAXS>
+__device__ __forceinline__ double grid_point(double ta, double tb) {
+  const int lane = threadIdx.x & 31;
+  return (lane == 31) ? tb : ta + (tb - ta) * (double)lane / 31.0;
+}
+
 // _best_candidate: round-robin candidates over lanes. A warm-start round evaluates 32 candidates
-// spread over the candidate range exactly; every other candidate is evaluated exactly only when a
-// rigorous lower bound on its cost does not exceed the best cost so far + 1e-15. A skipped
-// candidate therefore costs more than the final minimum + 1e-15: neither the minimum nor a tie.
-//
-// The bound of a certified breakpoint tau = et_g(m) (count_g(tau) == m, tb.gex): cost =
-// (work/batch) E P with E >= et_g(m) = tau and P = sum_r pr_r count_r(tau), where
-//   * count_g(tau) = m;
-//   * count_r(tau) >= count_r(tau_max) for every r, tau_max = the round's largest candidate
-//     (counts are non-increasing in tau): exact counts at tau_max are computed once per round,
-//     one stage per lane, and the warp sums them;
-//   * the top stage(s) also get a per-candidate FP32 lower bound (count_lb32).
-// All FP32 arithmetic of the bound is covered by a 1e-5 relative slack. tau_lo, tau_hi and
-// uncertified breakpoints are always evaluated.
+// around the grid minimiser of the convex bound L exactly (upper bound ub on the minimum). L
+// (lb_cont) then confines every certified breakpoint that could reach ub + 1e-15 to an
+// interval [ta, tb] (two grid levels, interval_cells); for each class leader those are the m in
+// [count(tb), count(ta)] (certified: count(et(m)) == m, counts non-increasing). Only these,
+// tau_lo, tau_hi and the uncertified breakpoints remain; each gets a per-candidate bound
+// (E >= tau, the generator's count m, the top stage's FP32 count bound, count(tau_hi) for the
+// others; FP32 slack 1e-5) and is evaluated exactly only when the bound does not exceed the best
+// cost so far + 1e-15. A skipped candidate costs more than the final minimum + 1e-15: it is
+// neither the minimum nor a tie.
 template <int MAXS>
 __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTables& tb,
                                         const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
@@ -223,7 +305,6 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     }
 #pragma unroll
     for (int q = 0; q < kTop; q++) sw.top[q] = t[q];
-
     HPS_STAT(ST_NCAND, n_cand);
     HPS_STAT(ST_PLANS_FAST, 1);
     HPS_STAT(ST_STAGES, S);
@@ -232,78 +313,138 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   const CostScalars cs{c.bo, c.batch, c.work, c.limit};
   TieBuf buf;
   buf.init();
-  const int rounds = (n_cand + 31) >> 5;
   int sp = 0;
-  {  // warm start: one round of 32 candidates spread evenly over the candidate range
-    const int i = (int)(((long long)lane * n_cand) >> 5);
-    int gen;
-    const double tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
+  const double C = c.work / c.batch;
+  // level-0 grid of the convex bound L over [tau_lo, tau_hi]
+  const bool grid = tau_hi > tau_lo;
+  double g_t = tau_lo, g_L = 0.0, g_d = 0.0;
+  if (grid) {
+    g_t = grid_point<MAXS>(tau_lo, tau_hi);
+    lb_cont<MAXS>(w, sw, S, c.bo, C, g_t, g_L, g_d);
+  }
+  {  // warm start: 32 certified breakpoints around the grid minimiser of L (the optimum is
+     // usually there), else spread over the whole candidate range
+    double lmin = grid ? g_L : 0.0;
+    for (int o = 16; o; o >>= 1) lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+    const unsigned at = __ballot_sync(0xffffffffu, grid && g_L == lmin);
+    const double tstar = __shfl_sync(0xffffffffu, g_t, at ? __ffs(at) - 1 : 0);
+    // leaders with certified breakpoints, their count at tstar
+    int cstar = 0;
+    bool ok = false;
+    if (lane < S) {
+      const int lo = sw.kmi[lane], chi = min(sw.kma[lane], sw.gex[lane]);
+      ok = grid && w.pre[lane + 1] > w.pre[lane] && chi >= lo;
+      if (ok) cstar = min(max(count_seeded(w.st[lane], w.row[lane], tstar, lo, sw.kma[lane]), lo), chi);
+    }
+    const unsigned lm = __ballot_sync(0xffffffffu, ok);
+    const int nl = __popc(lm);
+    double tau = -inf;
+    int gen = -1;
+    if (nl > 0) {
+      const int li = lane % nl, k = lane / nl;   // leader #li, offset 0, +1, -1, +2, -2, ...
+      const int r = __fns(lm, 0, li + 1);
+      const int cr = __shfl_sync(0xffffffffu, cstar, r);
+      const int off = (k & 1) ? (k + 1) >> 1 : -(k >> 1);
+      const int m = cr + off;
+      if (r < S && m >= sw.kmi[r] && m <= min(sw.kma[r], sw.gex[r])) {
+        gen = (r << 16) | m;
+        tau = __ldg(&w.row[r][m - 1].et);
+      }
+    } else {
+      const int i = (int)(((long long)lane * n_cand) >> 5);
+      tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
+    }
     if (tau >= tau_lo && tau <= tau_hi) {
       HPS_STAT(ST_CANDS, 1);
       buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau, gen), tau);
     }
   }
   double ub = warp_min(buf.mn);
-  const float fC = (float)(c.work / c.batch);
-#if !HPS_ROUNDB
-  float pl0 = 0.0f;  // counts at tau_hi
-  for (int r = lane; r < S; r += 32) {
-    sw.kr[r] = sw.kmi[r];
-    pl0 += sw.fpr[r] * (float)sw.kmi[r];
+  // ---- interval of the certified breakpoints that can still reach ub + 1e-15 ----
+  double ta = tau_lo, tbh = tau_hi;
+  if (grid && ub < inf) {
+    const double thr = (ub + 1e-15) * (1.0 + 1e-7);
+    interval_cells(g_t, g_L, g_d, thr, ta, tbh);
+    if (ta <= tbh) {
+      const double t1 = grid_point<MAXS>(ta, tbh);
+      double L1, d1;
+      lb_cont<MAXS>(w, sw, S, c.bo, C, t1, L1, d1);
+      interval_cells(t1, L1, d1, thr, ta, tbh);
+    }
   }
+  {
+    int cnt[2] = {0, 0};
+#pragma unroll
+    for (int slot = 0; slot < 2; slot++) {
+      const int r = lane + 32 * slot;
+      if (r < S && w.pre[r + 1] > w.pre[r]) {  // class leader with breakpoints
+        const int lo = sw.kmi[r], hi = sw.kma[r];
+        int alo = 0, an = 0;
+        const int chi = min(hi, sw.gex[r]);   // certified part [lo, chi]
+        if (ta <= tbh && chi >= lo) {
+          const int ma = count_seeded(w.st[r], w.row[r], tbh, lo, hi);  // smallest certified m
+          const int mb = count_seeded(w.st[r], w.row[r], ta, lo, hi);   // largest certified m
+          alo = max(ma, lo);
+          an = max(0, min(mb, chi) - alo + 1);
+        }
+        const int blo = max(lo, sw.gex[r] + 1);
+        sw.alo[r] = alo;
+        sw.an[r] = an;
+        sw.blo[r] = blo;
+        cnt[slot] = an + max(0, hi - blo + 1);
+      } else if (r < S) {
+        sw.an[r] = 0;
+        sw.blo[r] = 1;
+        cnt[slot] = 0;
+      }
+    }
+    int inc0 = cnt[0];
+    for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, inc0, o); if (lane >= o) inc0 += v; }
+    const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+    int inc1 = cnt[1];
+    for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, inc1, o); if (lane >= o) inc1 += v; }
+    const int tot1 = __shfl_sync(0xffffffffu, inc1, 31);
+    if (lane < S) sw.pre2[lane] = inc0 - cnt[0];
+    if (lane + 32 < S) sw.pre2[lane + 32] = tot0 + inc1 - cnt[1];
+    if (lane == 0) sw.pre2[S] = tot0 + tot1;
+    __syncwarp();
+  }
+  const int n2 = 2 + sw.pre2[S];
+  const float fC = (float)(c.work / c.batch);
+  float pl0 = 0.0f;  // sum of pr count(tau_hi)
+  for (int r = lane; r < S; r += 32) pl0 += sw.fpr[r] * (float)sw.kmi[r];
   for (int o = 16; o; o >>= 1) pl0 += __shfl_xor_sync(0xffffffffu, pl0, o);
-  __syncwarp();
-#endif
   int top[kTop > 0 ? kTop : 1];
 #pragma unroll
   for (int q = 0; q < kTop; q++) top[q] = sw.top[q];
-  // every candidate: lower-bound filter; survivors are compacted into sw.q and evaluated
-  // densely (a warp only saves work when all 32 lanes skip, so skipping must be compacted).
-  // A warm-start candidate may pass again; re-inserting it is harmless (same cost and tau).
+  // per-candidate filter; survivors are compacted into sw.q and evaluated densely (a warp only
+  // saves work when all 32 lanes skip, so skipping must be compacted). A warm-start candidate
+  // may pass again; re-inserting it is harmless (same cost and tau).
   sp = 0;
   int qn = 0;
   const unsigned lt = (1u << lane) - 1u;
+  const int rounds = (n2 + 31) >> 5;
   for (int jr = 0; jr < rounds; jr++) {
     const int i = jr * 32 + lane;
     double tau = 0.0;
     int gen = -1;
-    bool inr = false;
-    if (i < n_cand) {
-      tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
-      inr = tau >= tau_lo && tau <= tau_hi;
-    }
-    const double tmax = warp_max(inr ? tau : -inf);
-    if (!(tmax > -inf)) continue;  // warp-uniform
-#if HPS_ROUNDB
-    float pl = 0.0f;
-    for (int r = lane; r < S; r += 32) {
-      int k = sw.kmi[r];
-      double et_unused;
-      if (sw.kma[r] != k) {
-        const int k0 = count_est<MAXS>(w, sw, r, (float)tmax);
-        k = count_verify<MAXS>(w, sw, r, tmax, k0, te_pair(w.row[r], k0), te_theta(w.row[r], k0), et_unused);
-      }
-      sw.kr[r] = k;
-      pl += sw.fpr[r] * (float)k;
-    }
-    for (int o = 16; o; o >>= 1) pl += __shfl_xor_sync(0xffffffffu, pl, o);
-    __syncwarp();
-#else
-    const float pl = pl0;
-#endif
-    bool keep = inr;
-    if (inr && gen >= 0) {
-      const int g = gen >> 16, m = gen & 0xffff;
-      const float tf = (float)tau;
-      float P = pl + sw.fpr[g] * (float)(m - sw.kr[g]);
+    bool keep = false;
+    if (i < n2) {
+      tau = cand_tau2<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
+      keep = tau >= tau_lo && tau <= tau_hi;
+      if (keep && gen >= 0) {
+        const int g = gen >> 16, m = gen & 0xffff;
+        const float tf = (float)tau;
+        float P = pl0 + sw.fpr[g] * (float)(m - sw.kmi[g]);
 #pragma unroll
-      for (int q = 0; q < kTop; q++) {
-        const int r = top[q];
-        if (r < 0 || r == g) continue;
-        const int d = count_lb32(w.st[r], tf, sw.dom[r]) - sw.kr[r];
-        if (d > 0) P += sw.fpr[r] * (float)d;
+        for (int q = 0; q < kTop; q++) {
+          const int r = top[q];
+          if (r < 0 || r == g) continue;
+          const int d = count_lb32(w.st[r], tf, sw.dom[r]) - sw.kmi[r];
+          if (d > 0) P += sw.fpr[r] * (float)d;
+        }
+        keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > ub + 1e-15);
       }
-      keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > ub + 1e-15);
     }
     const unsigned mk = __ballot_sync(0xffffffffu, keep);
     if (keep) { sw.q[qn + __popc(mk & lt)] = tau; sw.qg[qn + __popc(mk & lt)] = gen; }
@@ -333,9 +474,9 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   if (__any_sync(0xffffffffu, buf.overflow)) {  // rare: exact second pass with the final limit
     bt = -inf;
     sp = 0;
-    for (int i = lane; i < n_cand; i += 32) {
+    for (int i = lane; i < n2; i += 32) {
       int gen;
-      const double tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
+      const double tau = cand_tau2<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
       if (!(tau >= tau_lo && tau <= tau_hi) || !(tau > bt)) continue;
       if (cost_exact<MAXS>(cs, w, sw, S, tau, gen) <= lim) bt = tau;
     }
