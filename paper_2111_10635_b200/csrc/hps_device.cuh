@@ -140,7 +140,7 @@ static __device__ HPS_NOINLINE_RARE int count_cert1(double frac, double omf, dou
 // sign of N that holds with margin at both ends holds on the whole interval; the margin
 // (relative 1e-9, far above the rounding of h and q) makes the reference's rounded q's obey
 // the same order, and iceil is monotone, so max(iceil(q_o), iceil(q_d)) = iceil(q_dominant).
-__device__ __forceinline__ int side_dominance(const StageEntry& s, double tlo, double thi, double bo) {
+static __device__ __noinline__ int side_dominance(const StageEntry& s, double tlo, double thi, double bo) {
   if (s.odt == 0.0) return (s.oct != 0.0 && s.alpha > 0.0) ? 1 : 0;
   if (s.oct == 0.0) return (s.beta > 0.0) ? 2 : 0;
   if (!(s.alpha > 0.0) || !(s.beta > 0.0)) return 0;

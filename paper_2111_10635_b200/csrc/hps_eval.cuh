@@ -54,7 +54,7 @@ struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min
   bool overflow;
   double mn;
   __device__ __forceinline__ void init() { n = 0; overflow = false; mn = __longlong_as_double(0x7ff0000000000000LL); }
-  __device__ HPS_NOINLINE void insert(double cost, double tau) {
+  __device__ __noinline__ void insert(double cost, double tau) {
     if (!(cost <= mn + 1e-15) && n > 0) return;  // cannot be within 1e-15 of the minimum
     if (cost < mn) {
       mn = cost;
@@ -83,12 +83,13 @@ struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min
   }
 };
 
+// (operands are never NaN: plain compares instead of fmax/fmin's NaN handling)
 __device__ __forceinline__ double warp_max(double v) {
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o; o >>= 1) { const double u = __shfl_xor_sync(0xffffffffu, v, o); v = (u > v) ? u : v; }
   return v;
 }
 __device__ __forceinline__ double warp_min(double v) {
-  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o; o >>= 1) { const double u = __shfl_xor_sync(0xffffffffu, v, o); v = (u < v) ? u : v; }
   return v;
 }
 __device__ __forceinline__ int warp_sum_i(int v) {
@@ -335,7 +336,7 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
 
 // Exact count(tau) of a stage known to lie in [lo, hi] (hi <= table cap): FP32 seed, confirmed by
 // theta(k) <= tau < theta(k - 1) or corrected by the galloping table search.
-__device__ __forceinline__ int count_seeded(const StageEntry& s, const TEPair* row, double tau, int lo, int hi) {
+static __device__ __noinline__ int count_seeded(const StageEntry& s, const TEPair* row, double tau, int lo, int hi) {
   const float tf = (float)tau;
   float q = 1.0f;
 #pragma unroll
@@ -803,7 +804,7 @@ __device__ double phase_candidates(const InstanceConsts& c, const DeviceTables& 
 // Phase C: counts at the chosen tau, add_ps_cores (ls/provisioner.py:486-513) and the final
 // evaluate() whose monetary_cost is the score (ls/scoring.py:96-97, ls/costmodel.py:102-167).
 template <int MAXS, bool FAST = false>
-__device__ void phase_final(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
+__device__ __noinline__ void phase_final(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
                             int S, double tau, PlanOut& out) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
@@ -864,7 +865,84 @@ __device__ void phase_final(const InstanceConsts& c, const DeviceTables& tb, War
         if (order[j] == t) { tot[j] += ps; break; }
     }
     double per_second = 0.0;
-    for (int j = 0; j < n; j++) per_second += c.price_h[order[j]] / 3600.0 * (double)tot[j];
+    for (int j = 0; j < n; j++) per_second += c.price_s[order[j]] * (double)tot[j];  // price / 3600.0
+    cost = exec_time * per_second;
+  }
+  out.cost = __shfl_sync(0xffffffffu, cost, 0);
+  out.status = HPS_ST_OK;
+  out.gap = 0.0;
+  out.ps = ps;
+}
+
+// Phase C on the fast path (quotas <= the table cap, so every count and per-type total fits 32
+// bits): counts at the chosen tau from the tables, add_ps_cores (ls/provisioner.py:486-513) and
+// evaluate()'s monetary cost (ls/costmodel.py:102-167) with per_type_totals in insertion order
+// (ls/domain.py:342-348). One compact out-of-line copy (runs once per plan).
+template <int MAXS>
+__device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, WarpSmem<MAXS>& w, int S, double tau,
+                                                 PlanOut& out) {
+  const int lane = threadIdx.x & 31;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  int accel = 0, on_ps = 0;
+  double emax = 0.0;
+#pragma unroll 1
+  for (int s = lane; s < S; s += 32) {
+    const int lo = (int)w.kmin[s], hi = (int)w.kmax[s];
+    const int k = (lo == hi) ? lo : count_seeded(w.st[s], w.row[s], tau, lo, hi);
+    w.kres[s] = (double)k;
+    const int t = w.st[s].type;
+    if (!c.is_cpu[t]) accel += k;
+    if (t == c.ps_type) on_ps += k;
+    const double et = __ldg(&w.row[s][k - 1].et);
+    emax = (et > emax) ? et : emax;
+  }
+  accel = (int)__reduce_add_sync(0xffffffffu, (unsigned)accel);
+  on_ps = (int)__reduce_add_sync(0xffffffffu, (unsigned)on_ps);
+  emax = warp_max(emax);
+  int ps = 0;
+  if (c.with_ps && accel != 0) {
+    if (c.ps_type < 0) { out.status = HPS_ST_NO_CPU_TYPE; out.cost = __longlong_as_double(0x7ff8000000000000LL); out.gap = 0; return; }
+    ps = (int)ceil(c.ps_cores_per_gpu * (double)accel - 1e-9);
+    const long long would = (long long)on_ps + ps;
+    if (would > c.quota[c.ps_type]) {
+      out.status = HPS_ST_PS_QUOTA;
+      out.gap = clamp_gap((double)(would - c.quota[c.ps_type]) / (double)c.quota[c.ps_type]);
+      out.cost = c.penalty_scale * (1.0 + pmax(0.0, out.gap));
+      return;
+    }
+  }
+  // evaluate(): overall = min_s B/et_s = B/max_s et_s (division is monotone); zero-time stages
+  // give inf (ls/costmodel.py:127-128)
+  const double overall = (emax > 0) ? c.batch / emax : inf;
+  const double exec_time = (overall > 0 && overall != inf) ? c.work / overall : 0.0;
+  // per-type totals; the sum runs over types in order of first occurrence, then the PS type
+#pragma unroll 1
+  for (int t = 0; t < c.T; t++) {
+    unsigned v = 0;
+#pragma unroll 1
+    for (int s = lane; s < S; s += 32) v += (w.st[s].type == t) ? (unsigned)w.kres[s] : 0u;
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (lane == 0) w.tsum[t] = v;
+  }
+  __syncwarp();
+  double cost = 0.0;
+  if (lane == 0) {
+    double per_second = 0.0;
+    unsigned seen = 0;
+    bool first = true;
+#pragma unroll 1
+    for (int s = 0; s < S; s++) {
+      const int t = w.st[s].type;
+      if (seen >> t & 1u) continue;
+      seen |= 1u << t;
+      const double term = c.price_s[t] * (double)(w.tsum[t] + (t == c.ps_type ? (unsigned long long)ps : 0ull));
+      per_second = first ? term : per_second + term;
+      first = false;
+    }
+    if (ps > 0 && !(seen >> c.ps_type & 1u)) {
+      const double term = c.price_s[c.ps_type] * (double)ps;
+      per_second = first ? term : per_second + term;
+    }
     cost = exec_time * per_second;
   }
   out.cost = __shfl_sync(0xffffffffu, cost, 0);

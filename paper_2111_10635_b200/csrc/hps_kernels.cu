@@ -891,7 +891,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Outpu
       r.gap = 1.0;
       r.cost = c.penalty_scale * (1.0 + 1.0);
     } else {
-      phase_final<MAXS, true>(c, tb, w, S, tau, r);
+      phase_final_fast<MAXS>(c, w, S, tau, r);
     }
     if (!ARGMIN) {
       write_plan<MAXS>(c, w, o, ps.p, r);

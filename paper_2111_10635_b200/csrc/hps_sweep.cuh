@@ -129,6 +129,13 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<M
   return cs.work / thr * P;
 }
 
+// exact cost of one candidate into the lane's tie buffer (one out-of-line copy for every site)
+template <int MAXS>
+__device__ __noinline__ void eval_insert(const CostScalars cs, const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
+                                         int S, double tau, int gen, TieBuf& buf) {
+  buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau, gen), tau);
+}
+
 // FP32 lower bound on count(tau) of an unpinned stage (pruning only). Every FP32 input and
 // operation carries a relative error of a few 2^-24; with kappa = B/h the headroom's relative
 // error is <= 3e-7 kappa + 6e-8, so q~ = frac/h~ is within q (1 +- e0), e0 = 4e-7 (kappa + 2).
@@ -197,7 +204,7 @@ __device__ __forceinline__ double cand_tau2(const WarpSmem<MAXS>& w, const Sweep
 // functions of tau (tau q(tau) = (frac/b)(1 + c/(b tau - c)) with c = 1 - frac), so L is convex.
 // Returns L and a subgradient dL/dtau at tau.
 template <int MAXS>
-__device__ __forceinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int S, double bo,
+__device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int S, double bo,
                                         double C, double tau, double& L, double& dL) {
   double P = 0.0, dP = 0.0;
   for (int r = 0; r < S; r++) {
@@ -229,7 +236,7 @@ __device__ __forceinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem
 // 31 = tb). On each cell, convexity bounds L from below by max(tangent at the left end, tangent
 // at the right end); [ta, tb] shrinks to the cells whose bound does not exceed thr (ta > tb when
 // none does).
-__device__ __forceinline__ void interval_cells(double t, double L, double d, double thr, double& ta, double& tb) {
+static __device__ __noinline__ void interval_cells(double t, double L, double d, double thr, double& ta, double& tb) {
   const int lane = threadIdx.x & 31;
   const double t1 = __shfl_down_sync(0xffffffffu, t, 1);
   const double L1 = __shfl_down_sync(0xffffffffu, L, 1);
@@ -256,6 +263,21 @@ __device__ __forceinline__ double grid_point(double ta, double tb) {
   return (lane == 31) ? tb : ta + (tb - ta) * (double)lane / 31.0;
 }
 
+// tie buffer overflow (rare): the largest tau of the restricted list whose exact cost is <= lim
+template <int MAXS>
+__device__ __noinline__ double overflow_pass(const CostScalars cs, const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
+                                             int S, double tau_lo, double tau_hi, int n2, double lim) {
+  double bt = -__longlong_as_double(0x7ff0000000000000LL);
+  int sp = 0;
+  for (int i = (threadIdx.x & 31); i < n2; i += 32) {
+    int gen;
+    const double tau = cand_tau2<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
+    if (!(tau >= tau_lo && tau <= tau_hi) || !(tau > bt)) continue;
+    if (cost_exact<MAXS>(cs, w, sw, S, tau, gen) <= lim) bt = tau;
+  }
+  return bt;
+}
+
 // _best_candidate: round-robin candidates over lanes. A warm-start round evaluates 32 candidates
 // around the grid minimiser of the convex bound L exactly (upper bound ub on the minimum). L
 // (lb_cont) then confines every certified breakpoint that could reach ub + 1e-15 to an
@@ -272,6 +294,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
                                         double tau_lo, double tau_hi, int n_cand) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll 1
   for (int r = lane; r < S; r += 32) {
     const bool pinned = (w.kmax[r] == w.kmin[r]);
     sw.pr[r] = c.price_s[w.st[r].type];
@@ -291,6 +314,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     double v[kTop > 0 ? kTop : 1];
 #pragma unroll
     for (int q = 0; q < kTop; q++) { t[q] = -1; v[q] = -1.0; }
+#pragma unroll 1
     for (int r = 0; r < S; r++) {
       if (w.kmax[r] == w.kmin[r]) continue;
       double vv = sw.pr[r] * (w.kmax[r] - w.kmin[r]);
@@ -325,7 +349,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   {  // warm start: 32 certified breakpoints around the grid minimiser of L (the optimum is
      // usually there), else spread over the whole candidate range
     double lmin = grid ? g_L : 0.0;
-    for (int o = 16; o; o >>= 1) lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+    lmin = warp_min(lmin);
     const unsigned at = __ballot_sync(0xffffffffu, grid && g_L == lmin);
     const double tstar = __shfl_sync(0xffffffffu, g_t, at ? __ffs(at) - 1 : 0);
     // leaders with certified breakpoints, their count at tstar
@@ -356,7 +380,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     }
     if (tau >= tau_lo && tau <= tau_hi) {
       HPS_STAT(ST_CANDS, 1);
-      buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau, gen), tau);
+      eval_insert<MAXS>(cs, w, sw, S, tau, gen, buf);
     }
   }
   double ub = warp_min(buf.mn);
@@ -410,8 +434,9 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     __syncwarp();
   }
   const int n2 = 2 + sw.pre2[S];
-  const float fC = (float)(c.work / c.batch);
+  const float fC = (float)C;
   float pl0 = 0.0f;  // sum of pr count(tau_hi)
+#pragma unroll 1
   for (int r = lane; r < S; r += 32) pl0 += sw.fpr[r] * (float)sw.kmi[r];
   for (int o = 16; o; o >>= 1) pl0 += __shfl_xor_sync(0xffffffffu, pl0, o);
   int top[kTop > 0 ? kTop : 1];
@@ -454,7 +479,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
       const double t = sw.q[qn - 32 + lane];
       const int tg = sw.qg[qn - 32 + lane];
       HPS_STAT(ST_CANDS, 1);
-      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t, tg), t);
+      eval_insert<MAXS>(cs, w, sw, S, t, tg, buf);
       qn -= 32;
       ub = fmin(ub, warp_min(buf.mn));
       __syncwarp();
@@ -464,7 +489,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     if (lane < qn) {
       const double t = sw.q[lane];
       HPS_STAT(ST_CANDS, 1);
-      buf.insert(cost_exact<MAXS>(cs, w, sw, S, t, sw.qg[lane]), t);
+      eval_insert<MAXS>(cs, w, sw, S, t, sw.qg[lane], buf);
     }
   }
   const double mf = warp_min(buf.mn);
@@ -472,14 +497,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   const double lim = mf + 1e-15;
   double bt;
   if (__any_sync(0xffffffffu, buf.overflow)) {  // rare: exact second pass with the final limit
-    bt = -inf;
-    sp = 0;
-    for (int i = lane; i < n2; i += 32) {
-      int gen;
-      const double tau = cand_tau2<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
-      if (!(tau >= tau_lo && tau <= tau_hi) || !(tau > bt)) continue;
-      if (cost_exact<MAXS>(cs, w, sw, S, tau, gen) <= lim) bt = tau;
-    }
+    bt = overflow_pass<MAXS>(cs, w, sw, S, tau_lo, tau_hi, n2, lim);
   } else {
     bt = buf.best_tau(lim);
   }
@@ -515,7 +533,7 @@ __device__ void eval_plan_fast(const InstanceConsts& c, const DeviceTables& tb, 
 #ifdef HPS_STATS
   const long long t3 = clock64();
 #endif
-  phase_final<MAXS, true>(c, tb, w, out.S, tau, out);
+  phase_final_fast<MAXS>(c, w, out.S, tau, out);
 #ifdef HPS_STATS
   if ((threadIdx.x & 31) == 0) HPS_STAT(ST_CYC_C, clock64() - t3);
 #endif
