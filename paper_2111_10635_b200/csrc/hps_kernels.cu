@@ -848,15 +848,83 @@ stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src
 #ifndef HPS_CAND_MINB
 #define HPS_CAND_MINB 32
 #endif
+// Per-plan result of cand_prep carried from prep_kernel to candidate_kernel.
+template <int MAXS>
+struct PrepState {
+  double ub;
+  int32_t top;
+  int8_t dom[MAXS], lead[MAXS];
+  int16_t alo[MAXS], an[MAXS], blo[MAXS];
+};
+
+// load PlanState q into the warp's shared-memory view; per-stage constants of the sweep
+template <int MAXS>
+__device__ __forceinline__ void load_state(const InstanceConsts& c, const DeviceTables& tb, const PlanState<MAXS>& ps,
+                                           WarpSmem<MAXS>& w) {
+  const int lane = threadIdx.x & 31;
+  const int S = ps.S;
+#pragma unroll 1
+  for (int s = lane; s < S; s += 32) {
+    const int e = ps.ent[s];
+    const StageEntry st = tb.stages[e];
+    w.st[s] = st;
+    w.ent[s] = e;
+    w.row[s] = tb.te + c.te_off[st.type] + (int64_t)(e - st.type * c.P) * (int64_t)(c.et_cap[st.type] + 1);
+    w.kmin[s] = (double)ps.kmin[s];
+    w.kmax[s] = (double)ps.kmax[s];
+    w.cls[s] = tb_class(tb, e);
+  }
+  for (int s = lane; s <= S; s += 32) w.pre[s] = ps.pre[s];
+  __syncwarp();
+}
+
+// K1b: per-plan sweep constants, warm start, bound interval and restricted candidate ranges
+template <int MAXS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, HPS_CAND_MINB / WARPS)
+prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<MAXS>* prep) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
+  SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmem<MAXS>) * WARPS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem<MAXS>& w = sm[warp];
+  SweepSmem<MAXS>& sw = ss[warp];
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
+  const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
+  const unsigned int n = *cont.count;
+  for (uint64_t q = gw; q < n; q += nw) {
+    const PlanState<MAXS>& ps = states[q];
+    load_state<MAXS>(c, tb, ps, w);
+    const int S = ps.S;
+    TieBuf buf;
+    buf.init();
+    const double ub = cand_prep<MAXS>(c, tb, w, sw, S, ps.tau_lo, ps.tau_hi, ps.n_cand, buf);
+    PrepState<MAXS>& out = prep[q];
+    for (int s = lane; s < S; s += 32) {
+      out.dom[s] = (int8_t)sw.dom[s];
+      out.lead[s] = sw.lead[s];
+      out.alo[s] = (int16_t)sw.alo[s];
+      out.an[s] = (int16_t)sw.an[s];
+      out.blo[s] = (int16_t)sw.blo[s];
+    }
+    if (lane == 0) {
+      out.ub = ub;
+      out.top = sw.top[0];
+    }
+    __syncwarp();
+  }
+}
+
+// K1c: filter + exact evaluation over the restricted list, add_ps_cores, final cost, argmin
 template <int MAXS, int WARPS, bool ARGMIN>
 __global__ void __launch_bounds__(WARPS * 32, HPS_CAND_MINB / WARPS)
-candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Outputs o,
+candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const PrepState<MAXS>* prep, Outputs o,
                  int feasible_only, KeyPart* parts, int first) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
   SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmem<MAXS>) * WARPS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSmem<MAXS>& w = sm[warp];
+  SweepSmem<MAXS>& sw = ss[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
   const unsigned int n = *cont.count;
@@ -868,24 +936,32 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Outpu
   uint32_t flags = 0;
   for (uint64_t q = gw; q < n; q += nw) {
     const PlanState<MAXS>& ps = states[q];
+    load_state<MAXS>(c, tb, ps, w);
     const int S = ps.S;
-    for (int s = lane; s < S; s += 32) {
-      const int e = ps.ent[s];
-      const StageEntry st = tb.stages[e];
-      w.st[s] = st;
-      w.ent[s] = e;
-      w.row[s] = tb.te + c.te_off[st.type] + (int64_t)(e - st.type * c.P) * (int64_t)(c.et_cap[st.type] + 1);
-      w.kmin[s] = (double)ps.kmin[s];
-      w.kmax[s] = (double)ps.kmax[s];
-      w.cls[s] = tb_class(tb, e);
+    const PrepState<MAXS>& pp = prep[q];
+#pragma unroll 1
+    for (int r = lane; r < S; r += 32) {
+      const int lo = ps.kmin[r], hi = ps.kmax[r];
+      sw.pr[r] = c.price_s[w.st[r].type];
+      sw.fpr[r] = (float)sw.pr[r];
+      sw.kmi[r] = lo;
+      sw.kma[r] = hi;
+      sw.etp[r] = (lo == hi) ? __ldg(&w.row[r][lo - 1].et) : 0.0;
+      sw.dom[r] = pp.dom[r];
+      sw.lead[r] = pp.lead[r];
+      sw.alo[r] = pp.alo[r];
+      sw.an[r] = pp.an[r];
+      sw.blo[r] = pp.blo[r];
     }
-    for (int s = lane; s <= S; s += 32) w.pre[s] = ps.pre[s];
+    if (lane == 0) sw.top[0] = pp.top;
     __syncwarp();
     PlanOut r;
     r.ps = 0;
     r.gap = 0.0;
     r.S = S;
-    const double tau = phase_candidates_fast<MAXS>(c, tb, w, ss[warp], S, ps.tau_lo, ps.tau_hi, ps.n_cand);
+    TieBuf buf;
+    buf.init();
+    const double tau = cand_main<MAXS>(c, w, sw, S, ps.tau_lo, ps.tau_hi, pp.ub, buf);
     if (tau != tau) {
       r.status = HPS_ST_NO_CANDIDATE;
       r.gap = 1.0;
@@ -961,11 +1037,15 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
               int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
   const uint64_t chunk = std::min<uint64_t>(n, MAXS <= 16 ? (4ull << 20) : (MAXS <= 32 ? (2ull << 20) : (1ull << 20)));
   char* buf = nullptr;
-  CUDA_TRY(cudaMallocAsync(&buf, sizeof(PlanState<MAXS>) * chunk + 256, st));
+  const size_t state_bytes = (sizeof(PlanState<MAXS>) * chunk + 255) / 256 * 256;
+  CUDA_TRY(cudaMallocAsync(&buf, state_bytes + sizeof(PrepState<MAXS>) * chunk + 256, st));
   Cont cont{buf + 256, reinterpret_cast<unsigned int*>(buf)};
+  PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(buf + 256 + state_bytes);
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
   const size_t smem2 = (sizeof(WarpSmem<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
+  auto kp = prep_kernel<MAXS, WARPS>;
+  CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
   if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
@@ -979,7 +1059,10 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     if (rc) return rc;
     HPS_COUNT_LAUNCH();
-    k2<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, o, feasible_only, parts_b, first);
+    kp<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, prep);
+    CUDA_TRY(cudaGetLastError());
+    HPS_COUNT_LAUNCH();
+    k2<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaFreeAsync(buf, st));

@@ -288,10 +288,14 @@ __device__ __noinline__ double overflow_pass(const CostScalars cs, const WarpSme
 // others; FP32 slack 1e-5) and is evaluated exactly only when the bound does not exceed the best
 // cost so far + 1e-15. A skipped candidate costs more than the final minimum + 1e-15: it is
 // neither the minimum nor a tie.
+// Part 1 (cand_prep): per-plan constants, warm start, interval and restricted ranges (alo, an,
+// blo); returns ub. Part 2 (cand_main): the filter and exact evaluation over the restricted list.
+// The split path runs them in separate kernels (instruction-cache footprint): part 2 then starts
+// with an empty tie buffer, which loses nothing, because every warm-start candidate that can be
+// the minimum or a tie (cost <= ub + 1e-15) lies in the restricted list and passes the filter.
 template <int MAXS>
-__device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTables& tb,
-                                        const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
-                                        double tau_lo, double tau_hi, int n_cand) {
+__device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, const WarpSmem<MAXS>& w,
+                            SweepSmem<MAXS>& sw, int S, double tau_lo, double tau_hi, int n_cand, TieBuf& buf) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll 1
@@ -335,8 +339,6 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   }
   __syncwarp();
   const CostScalars cs{c.bo, c.batch, c.work, c.limit};
-  TieBuf buf;
-  buf.init();
   int sp = 0;
   const double C = c.work / c.batch;
   // level-0 grid of the convex bound L over [tau_lo, tau_hi]
@@ -397,7 +399,6 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     }
   }
   {
-    int cnt[2] = {0, 0};
 #pragma unroll
     for (int slot = 0; slot < 2; slot++) {
       const int r = lane + 32 * slot;
@@ -415,24 +416,47 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
         sw.alo[r] = alo;
         sw.an[r] = an;
         sw.blo[r] = blo;
-        cnt[slot] = an + max(0, hi - blo + 1);
       } else if (r < S) {
+        sw.alo[r] = 0;
         sw.an[r] = 0;
-        sw.blo[r] = 1;
-        cnt[slot] = 0;
+        sw.blo[r] = sw.kma[r] + 1;   // no breakpoints
       }
     }
-    int inc0 = cnt[0];
-    for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, inc0, o); if (lane >= o) inc0 += v; }
-    const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
-    int inc1 = cnt[1];
-    for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, inc1, o); if (lane >= o) inc1 += v; }
-    const int tot1 = __shfl_sync(0xffffffffu, inc1, 31);
-    if (lane < S) sw.pre2[lane] = inc0 - cnt[0];
-    if (lane + 32 < S) sw.pre2[lane + 32] = tot0 + inc1 - cnt[1];
-    if (lane == 0) sw.pre2[S] = tot0 + tot1;
-    __syncwarp();
   }
+  __syncwarp();
+  return ub;
+}
+
+// exclusive prefix of the restricted per-stage candidate counts an + (kmax - blo + 1)
+template <int MAXS>
+__device__ __forceinline__ void restricted_prefix(SweepSmem<MAXS>& sw, int S) {
+  const int lane = threadIdx.x & 31;
+  int cnt[2] = {0, 0};
+#pragma unroll
+  for (int slot = 0; slot < 2; slot++) {
+    const int r = lane + 32 * slot;
+    if (r < S) cnt[slot] = sw.an[r] + max(0, sw.kma[r] - sw.blo[r] + 1);
+  }
+  int inc0 = cnt[0];
+  for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, inc0, o); if (lane >= o) inc0 += v; }
+  const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+  int inc1 = cnt[1];
+  for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, inc1, o); if (lane >= o) inc1 += v; }
+  const int tot1 = __shfl_sync(0xffffffffu, inc1, 31);
+  if (lane < S) sw.pre2[lane] = inc0 - cnt[0];
+  if (lane + 32 < S) sw.pre2[lane + 32] = tot0 + inc1 - cnt[1];
+  if (lane == 0) sw.pre2[S] = tot0 + tot1;
+  __syncwarp();
+}
+
+template <int MAXS>
+__device__ double cand_main(const InstanceConsts& c, const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
+                            double tau_lo, double tau_hi, double ub, TieBuf& buf) {
+  const int lane = threadIdx.x & 31;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const CostScalars cs{c.bo, c.batch, c.work, c.limit};
+  restricted_prefix<MAXS>(sw, S);
+  const double C = c.work / c.batch;
   const int n2 = 2 + sw.pre2[S];
   const float fC = (float)C;
   float pl0 = 0.0f;  // sum of pr count(tau_hi)
@@ -442,6 +466,7 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
   int top[kTop > 0 ? kTop : 1];
 #pragma unroll
   for (int q = 0; q < kTop; q++) top[q] = sw.top[q];
+  int sp = 0;
   // per-candidate filter; survivors are compacted into sw.q and evaluated densely (a warp only
   // saves work when all 32 lanes skip, so skipping must be compacted). A warm-start candidate
   // may pass again; re-inserting it is harmless (same cost and tau).
@@ -502,6 +527,16 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
     bt = buf.best_tau(lim);
   }
   return warp_max(bt);
+}
+
+template <int MAXS>
+__device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTables& tb,
+                                        const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
+                                        double tau_lo, double tau_hi, int n_cand) {
+  TieBuf buf;
+  buf.init();
+  const double ub = cand_prep<MAXS>(c, tb, w, sw, S, tau_lo, tau_hi, n_cand, buf);
+  return cand_main<MAXS>(c, w, sw, S, tau_lo, tau_hi, ub, buf);
 }
 
 // Whole plan, fast path. Falls back to the literal path's pending marker for >4096 candidates.
