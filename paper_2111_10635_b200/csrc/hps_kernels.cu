@@ -47,6 +47,7 @@ int set_err(int code, const std::string& msg) {
 
 constexpr int kEtCapMax = 16384;
 constexpr int kSlowThreads = 256;
+constexpr int kSlowSmemSort = 8192;   // doubles of dynamic shared memory for the slow path's sort
 
 // ------------------------------------------------------------------ plan sources
 
@@ -371,6 +372,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
   __shared__ int s_ncand, s_S, s_done;
   __shared__ PlanOut s_out;
   __shared__ u128 s_rank;
+  extern __shared__ double s_sort[];  // kSlowSmemSort doubles: the sort runs here when it fits
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* raw = scratch + (size_t)blockIdx.x * per_block;  // [per_block/2] sort buffer
   double* cand = raw + per_block / 2;                       // distinct / kept candidates
@@ -400,6 +402,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       const int nraw = s_ncand;
       int npow = 1;
       while (npow < nraw) npow <<= 1;
+      double* srt = (npow <= kSlowSmemSort) ? s_sort : raw;  // sort buffer: shared memory if it fits
       // raw candidates (class leaders' breakpoints + tau_lo/tau_hi), out-of-range -> +inf
       for (int i = tid; i < npow; i += kSlowThreads) {
         double v = __longlong_as_double(0x7ff0000000000000LL);
@@ -413,18 +416,17 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
           v = et_lookup(c, tb, w.st[lo], w.ent[lo], w.kmin[lo] + (double)(j - w.pre[lo]));
           if (!(v >= tau_lo && v <= tau_hi)) v = __longlong_as_double(0x7ff0000000000000LL);
         }
-        raw[i] = v;
+        srt[i] = v;
       }
       __syncthreads();
-      for (int k = 2; k <= npow; k <<= 1)  // bitonic sort ascending
+      for (int k = 2; k <= npow; k <<= 1)  // bitonic sort ascending (one thread per pair)
         for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int i = tid; i < npow; i += kSlowThreads) {
-            const int l = i ^ j;
-            if (l > i) {
-              const double a = raw[i], b = raw[l];
-              const bool up = (i & k) == 0;
-              if (up ? (a > b) : (a < b)) { raw[i] = b; raw[l] = a; }
-            }
+          for (int t = tid; t < (npow >> 1); t += kSlowThreads) {
+            const int i = 2 * t - (t & (j - 1));   // lower index of pair t at distance j
+            const int l = i + j;
+            const double a = srt[i], b = srt[l];
+            const bool up = (i & k) == 0;
+            if (up ? (a > b) : (a < b)) { srt[i] = b; srt[l] = a; }
           }
           __syncthreads();
         }
@@ -433,11 +435,11 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       const int b0 = min(npow, tid * chunk), b1 = min(npow, b0 + chunk);
       unsigned cnt = 0;
       for (int i = b0; i < b1; i++)
-        if (raw[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || raw[i] != raw[i - 1])) cnt++;
+        if (srt[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || srt[i] != srt[i - 1])) cnt++;
       unsigned nc;
       unsigned at = block_excl_scan(cnt, scan_tmp, nc);
       for (int i = b0; i < b1; i++)
-        if (raw[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || raw[i] != raw[i - 1])) cand[at++] = raw[i];
+        if (srt[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || srt[i] != srt[i - 1])) cand[at++] = srt[i];
       __syncthreads();
       bool ovf = false;
       if (nc > (unsigned)kBpLimit) {  // ls/provisioner.py:456-470
@@ -1099,7 +1101,8 @@ int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending p
   const int blocks = (int)std::min<size_t>((size_t)in->sm_count * 2, cap_blocks);
   CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
   HPS_COUNT_LAUNCH();
-  slow_kernel<<<blocks, kSlowThreads, 0, st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
+  CUDA_TRY(cudaFuncSetAttribute(slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSlowSmemSort * sizeof(double))));
+  slow_kernel<<<blocks, kSlowThreads, kSlowSmemSort * sizeof(double), st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
                                                     slow_parts, scratch, per_block);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(scratch, st));
