@@ -366,8 +366,9 @@ __device__ __forceinline__ float q_cont(const StageEntry& s, float tau, float& d
     const float frac = side ? s.f_beta : s.f_alpha;
     if (rb == 0.0f || frac == 0.0f) continue;
     const float h = tau * rb - (side ? s.f_omb : s.f_oma);
-    const float v = (h > 0.0f) ? frac / h : 3.0e38f;
-    if (v > q) { q = v; dq = (h > 0.0f) ? -v * rb / h : -3.0e38f; }
+    const float rh = rcp_approx_f32(h);            // seed arithmetic: MUFU reciprocal
+    const float v = (h > 0.0f) ? frac * rh : 3.0e38f;
+    if (v > q) { q = v; dq = (h > 0.0f) ? -v * rb * rh : -3.0e38f; }
   }
   return q;
 }
@@ -443,7 +444,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
         dF += __shfl_xor_sync(0xffffffffu, dF, o);
       }
       if (fabsf(F - target) <= 0.25f || !(dF < 0.0f) || !(F < 3.0e37f)) break;
-      float nx = x + F * (1.0f - F / target) / dF;
+      float nx = x + F * (1.0f - __fdividef(F, target)) * rcp_approx_f32(dF);
       nx = fminf(fmaxf(nx, flo), fhi);
       const bool done = fabsf(nx - x) <= 1e-7f * x;
       x = nx;
