@@ -360,6 +360,9 @@ __device__ unsigned block_excl_scan(unsigned v, unsigned* tmp, unsigned& total) 
   return r;
 }
 
+// FAST: quotas within the threshold tables (HpsInstance::fast): the exact table-driven bisection
+// and final phase; otherwise the literal arithmetic of both.
+template <bool FAST>
 __global__ void __launch_bounds__(kSlowThreads)
 slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, Outputs o,
             Pending pend, int argmin_mode, int feasible_only, KeyPart* slow_parts,
@@ -389,7 +392,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       r.ps = 0; r.gap = 0.0;
       double tlo = 0, thi = 0;
       int ncand = 0;
-      const bool go = phase_stages_bisect<64>(c, tb, w, d0, d1, r, tlo, thi, ncand);
+      const bool go = phase_stages_bisect<64, FAST>(c, tb, w, d0, d1, r, tlo, thi, ncand);
       if (lane == 0) {
         s_out = r; s_tau_lo = tlo; s_tau_hi = thi; s_ncand = ncand; s_S = r.S; s_done = go ? 0 : 1;
         s_rank = rank;
@@ -522,7 +525,8 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
         if (!(mf < __longlong_as_double(0x7ff0000000000000LL))) {
           r.status = HPS_ST_NO_CANDIDATE; r.gap = 1.0; r.cost = c.penalty_scale * 2.0;
         } else {
-          phase_final<64>(c, tb, w, S, tau, r);
+          if (FAST) phase_final_fast<64>(c, w, S, tau, r);
+          else phase_final<64>(c, tb, w, S, tau, r);
         }
         if (ovf) r.status |= HPS_ST_OVERFLOW_FLAG;
         if (lane == 0) s_out = r;
@@ -1101,8 +1105,9 @@ int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending p
   const int blocks = (int)std::min<size_t>((size_t)in->sm_count * 2, cap_blocks);
   CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
   HPS_COUNT_LAUNCH();
-  CUDA_TRY(cudaFuncSetAttribute(slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSlowSmemSort * sizeof(double))));
-  slow_kernel<<<blocks, kSlowThreads, kSlowSmemSort * sizeof(double), st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
+  auto ks = in->fast ? slow_kernel<true> : slow_kernel<false>;
+  CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSlowSmemSort * sizeof(double))));
+  ks<<<blocks, kSlowThreads, kSlowSmemSort * sizeof(double), st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
                                                     slow_parts, scratch, per_block);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(scratch, st));
