@@ -551,10 +551,79 @@ __device__ __forceinline__ double candidate_cost(const InstanceConsts& c, const 
   return c.work / thr * P;
 }
 
+// m_min / m_max and class leaders (ls/provisioner.py:442-455): counts at tau_lo in kb (lane
+// slots), then the candidate count over class leaders (identical (oct, odt, alpha, beta) =>
+// identical counts and breakpoints, so only the first stage of a class contributes distinct
+// values) and its exclusive prefix in w.pre; n_cand includes tau_lo and tau_hi.
+template <int MAXS>
+__device__ __forceinline__ void cands_prefix(const DeviceTables& tb, WarpSmem<MAXS>& w, int S, const double kb[2],
+                                             int& n_cand) {
+  const int lane = threadIdx.x & 31;
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s < S) {
+      w.kmax[s] = kb[slot];
+      w.cls[s] = tb_class(tb, w.ent[s]);
+    }
+  }
+  __syncwarp();
+  int cnt[2] = {0, 0};
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s < S) {
+      bool leader = true;
+      for (int q = 0; q < s; q++)
+        if (w.cls[q] == w.cls[s]) { leader = false; break; }
+      double span = w.kmax[s] - w.kmin[s];
+      if (leader && span <= (double)kBpLimit) cnt[slot] = (int)span + 1;
+    }
+  }
+  // exclusive prefix over s = 0..S-1 (slot 0 then slot 1)
+  int inc0 = cnt[0];
+  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, inc0, o); if (lane >= o) inc0 += v; }
+  int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+  int inc1 = cnt[1];
+  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, inc1, o); if (lane >= o) inc1 += v; }
+  int tot1 = __shfl_sync(0xffffffffu, inc1, 31);
+  if (lane < S) w.pre[lane] = inc0 - cnt[0];
+  if (lane + 32 < S) w.pre[lane + 32] = tot0 + inc1 - cnt[1];
+  if (lane == 0) w.pre[S] = tot0 + tot1;
+  __syncwarp();
+  n_cand = tot0 + tot1 + 2;
+}
+
+// Fast-path bisection from the counts at tau_hi (w.kmin) on (serial, tau_hi), then the candidate
+// prefix. Needs w.st, w.ent, w.row, w.kmin.
+template <int MAXS>
+__device__ __forceinline__ void phase_bisect_cands(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
+                                                   int S, double a, double b, double& tau_lo_out, int& n_cand) {
+  const int lane = threadIdx.x & 31;
+  double kb[2] = {0.0, 0.0};
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s < S) kb[slot] = w.kmin[s];
+  }
+  int kl[2];
+#if HPS_BISECT_PROBES
+  b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
+#else
+  const double bd = bisect_direct(c, w.st, w.row, S, a, b, kb, kl);
+  if (bd == bd) b = bd;
+  else {  // (rare) seed too far off
+    if (lane == 0) HPS_STAT(ST_UNPINNED, 1);
+    b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
+  }
+#endif
+  kb[0] = (double)kl[0];
+  kb[1] = (double)kl[1];
+  tau_lo_out = b;
+  cands_prefix<MAXS>(tb, w, S, kb, n_cand);
+}
+
 // Phase A: stages, optimize_k1 exits and the bisection. Returns false when the plan is
 // finished (infeasible / invalid); otherwise fills w.kmin/kmax and tau_lo/tau_hi.
 // Lane l holds digits d0 (layer l) and d1 (layer l+32).
-template <int MAXS, bool FAST = false>
+template <int MAXS, bool FAST = false, bool HI_ONLY = false>
 __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables& tb,
                                     WarpSmem<MAXS>& w, int d0, int d1, PlanOut& out,
                                     double& tau_lo_out, double& tau_hi_out, int& n_cand) {
@@ -671,23 +740,19 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
     const int s = lane + 32 * slot;
     if (s < S) w.kmin[s] = kb[slot];
   }
+  tau_hi_out = tau_hi;
+  if (HI_ONLY) {  // split path: the bisection runs in its own kernel (bisect_kernel)
+    tau_lo_out = ser;
+    n_cand = 0;
+    return true;
+  }
   // --- bisection (ls/provisioner.py:430-437); counts monotone in tau => pinning ---
-  double a = ser, b = tau_hi;
   if (FAST) {
-    int kl[2];
-#if HPS_BISECT_PROBES
-    b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
-#else
-    const double bd = bisect_direct(c, w.st, w.row, S, a, b, kb, kl);
-    if (bd == bd) b = bd;
-    else {  // (rare) seed too far off
-      if ((threadIdx.x & 31) == 0) HPS_STAT(ST_UNPINNED, 1);
-      b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
-    }
-#endif
-    kb[0] = (double)kl[0];
-    kb[1] = (double)kl[1];
-  } else {
+    phase_bisect_cands<MAXS>(c, tb, w, S, ser, tau_hi, tau_lo_out, n_cand);
+    return true;
+  }
+  double a = ser, b = tau_hi;
+  {
     for (int it = 0; it < 60; it++) {
       const double mid = (a + b) / 2.0;
       double km[2] = {inf, inf};
@@ -708,43 +773,8 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
       else { a = mid; ka[0] = km[0]; ka[1] = km[1]; }
     }
   }
-  const double tau_lo = b;
-  // --- m_min / m_max and class leaders (ls/provisioner.py:442-455) ---
-  for (int slot = 0; slot < 2; slot++) {
-    const int s = lane + 32 * slot;
-    if (s < S) {
-      w.kmax[s] = kb[slot];
-      w.cls[s] = tb_class(tb, w.ent[s]);
-    }
-  }
-  __syncwarp();
-  // candidate count over class leaders (identical (oct,odt,alpha,beta) => identical counts
-  // and breakpoints, so only the first stage of a class contributes distinct values)
-  int cnt[2] = {0, 0};
-  for (int slot = 0; slot < 2; slot++) {
-    const int s = lane + 32 * slot;
-    if (s < S) {
-      bool leader = true;
-      for (int q = 0; q < s; q++)
-        if (w.cls[q] == w.cls[s]) { leader = false; break; }
-      double span = w.kmax[s] - w.kmin[s];
-      if (leader && span <= (double)kBpLimit) cnt[slot] = (int)span + 1;
-    }
-  }
-  // exclusive prefix over s = 0..S-1 (slot 0 then slot 1)
-  int inc0 = cnt[0];
-  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, inc0, o); if (lane >= o) inc0 += v; }
-  int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
-  int inc1 = cnt[1];
-  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, inc1, o); if (lane >= o) inc1 += v; }
-  int tot1 = __shfl_sync(0xffffffffu, inc1, 31);
-  if (lane < S) w.pre[lane] = inc0 - cnt[0];
-  if (lane + 32 < S) w.pre[lane + 32] = tot0 + inc1 - cnt[1];
-  if (lane == 0) w.pre[S] = tot0 + tot1;
-  __syncwarp();
-  n_cand = tot0 + tot1 + 2;
-  tau_lo_out = tau_lo;
-  tau_hi_out = tau_hi;
+  tau_lo_out = b;
+  cands_prefix<MAXS>(tb, w, S, kb, n_cand);
   return true;
 }
 

@@ -806,33 +806,25 @@ stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src
     double tau_lo, tau_hi;
     int n_cand;
     if (lane == 0) HPS_STAT(ST_PLANS, 1);
-    if (phase_stages_bisect<MAXS, true>(c, tb, w, d0, d1, r, tau_lo, tau_hi, n_cand)) {
-      if (n_cand > kBpLimit) {
-        if (lane == 0) {
-          HPS_STAT(ST_PENDING, 1);
-          const unsigned int at = atomicAdd(pend.count, 1u);
-          if (at < pend.cap) pend.list[at] = p;
-        }
-      } else {
-        unsigned int at = 0;
-        if (lane == 0) at = atomicAdd(cont.count, 1u);
-        at = __shfl_sync(0xffffffffu, at, 0);
-        PlanState<MAXS>& ps = states[at];
-        for (int s = lane; s < r.S; s += 32) {
-          ps.ent[s] = w.ent[s];
-          ps.kmin[s] = (int32_t)w.kmin[s];
-          ps.kmax[s] = (int32_t)w.kmax[s];
-        }
-        for (int s = lane; s <= r.S; s += 32) ps.pre[s] = w.pre[s];
-        if (lane == 0) {
-          ps.p = p;
-          ps.rank_hi = (uint64_t)(rank >> 64);
-          ps.rank_lo = (uint64_t)rank;
-          ps.tau_lo = tau_lo;
-          ps.tau_hi = tau_hi;
-          ps.S = r.S;
-          ps.n_cand = n_cand;
-        }
+    // up to the counts at tau_hi; the bisection runs in bisect_kernel (tau_lo holds the serial
+    // floor, the bisection's lower end, until then)
+    if (phase_stages_bisect<MAXS, true, true>(c, tb, w, d0, d1, r, tau_lo, tau_hi, n_cand)) {
+      unsigned int at = 0;
+      if (lane == 0) at = atomicAdd(cont.count, 1u);
+      at = __shfl_sync(0xffffffffu, at, 0);
+      PlanState<MAXS>& ps = states[at];
+      for (int s = lane; s < r.S; s += 32) {
+        ps.ent[s] = w.ent[s];
+        ps.kmin[s] = (int32_t)w.kmin[s];
+      }
+      if (lane == 0) {
+        ps.p = p;
+        ps.rank_hi = (uint64_t)(rank >> 64);
+        ps.rank_lo = (uint64_t)rank;
+        ps.tau_lo = tau_lo;
+        ps.tau_hi = tau_hi;
+        ps.S = r.S;
+        ps.n_cand = 0;
       }
     } else if (!ARGMIN) {
       write_plan<MAXS>(c, w, o, p, r);
@@ -854,6 +846,54 @@ stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src
 #ifndef HPS_CAND_MINB
 #define HPS_CAND_MINB 32
 #endif
+// K1a': the quota bisection (bisect_direct) and the candidate prefix of each surviving plan,
+// in place on its PlanState; plans with more than 4096 breakpoints go to the slow path and
+// are marked (n_cand = -1) for the kernels that follow.
+template <int MAXS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, HPS_STAGE_MINB / WARPS)
+bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending pend) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem<MAXS>& w = sm[warp];
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
+  PlanState<MAXS>* states = reinterpret_cast<PlanState<MAXS>*>(cont.states);
+  const unsigned int n = *cont.count;
+  for (uint64_t q = gw; q < n; q += nw) {
+    PlanState<MAXS>& ps = states[q];
+    const int S = ps.S;
+#pragma unroll 1
+    for (int s = lane; s < S; s += 32) {
+      const int e = ps.ent[s];
+      const StageEntry st = tb.stages[e];
+      w.st[s] = st;
+      w.ent[s] = e;
+      w.row[s] = tb.te + c.te_off[st.type] + (int64_t)(e - st.type * c.P) * (int64_t)(c.et_cap[st.type] + 1);
+      w.kmin[s] = (double)ps.kmin[s];
+    }
+    __syncwarp();
+    double tau_lo;
+    int n_cand;
+    phase_bisect_cands<MAXS>(c, tb, w, S, ps.tau_lo, ps.tau_hi, tau_lo, n_cand);
+    if (n_cand > kBpLimit) {
+      if (lane == 0) {
+        HPS_STAT(ST_PENDING, 1);
+        const unsigned int at = atomicAdd(pend.count, 1u);
+        if (at < pend.cap) pend.list[at] = ps.p;
+        ps.n_cand = -1;
+      }
+    } else {
+      for (int s = lane; s < S; s += 32) ps.kmax[s] = (int32_t)w.kmax[s];
+      for (int s = lane; s <= S; s += 32) ps.pre[s] = w.pre[s];
+      if (lane == 0) {
+        ps.tau_lo = tau_lo;
+        ps.n_cand = n_cand;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Per-plan result of cand_prep carried from prep_kernel to candidate_kernel.
 template <int MAXS>
 struct PrepState {
@@ -899,6 +939,7 @@ prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<
   const unsigned int n = *cont.count;
   for (uint64_t q = gw; q < n; q += nw) {
     const PlanState<MAXS>& ps = states[q];
+    if (ps.n_cand < 0) continue;  // slow path
     load_state<MAXS>(c, tb, ps, w);
     const int S = ps.S;
     TieBuf buf;
@@ -942,6 +983,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
   uint32_t flags = 0;
   for (uint64_t q = gw; q < n; q += nw) {
     const PlanState<MAXS>& ps = states[q];
+    if (ps.n_cand < 0) continue;  // slow path
     load_state<MAXS>(c, tb, ps, w);
     const int S = ps.S;
     const PrepState<MAXS>& pp = prep[q];
@@ -1050,6 +1092,9 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
   const size_t smem2 = (sizeof(WarpSmem<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
+  const size_t smem1 = sizeof(WarpSmem<MAXS>) * WARPS;
+  auto kb = bisect_kernel<MAXS, WARPS>;
+  CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
   auto kp = prep_kernel<MAXS, WARPS>;
   CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
@@ -1064,6 +1109,9 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     else if (src.mode == 1) rc = launch_stage<MAXS, WARPS, ARGMIN, 1>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     if (rc) return rc;
+    HPS_COUNT_LAUNCH();
+    kb<<<grid, WARPS * 32, smem1, st>>>(in->c, in->tb, cont, pend);
+    CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
     kp<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, prep);
     CUDA_TRY(cudaGetLastError());
