@@ -220,9 +220,11 @@ __device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MA
         const double cc = side ? s.omb : s.oma;
         const double h = tau * (bo * (side ? s.rwd : s.rwo)) - cc;
         if (!(h > 0.0)) { v = __longlong_as_double(0x7ff0000000000000LL); dv = 0.0; continue; }
-        const double q = frac * rcp_1nt(h);
+        const double rh = rcp_1nt(h);
+        const double q = frac * rh;
         const double vq = tau * (q * (1.0 - 1e-8) - 1e-9);
-        if (vq > v) { v = vq; dv = (1.0 - 1e-8) * (-q * q * cc / frac) - 1e-9; }
+        // d(tau q)/dtau = -q^2 c / frac = -q c / h
+        if (vq > v) { v = vq; dv = (1.0 - 1e-8) * (-q * cc * rh) - 1e-9; }
       }
     }
     P += sw.pr[r] * v;
@@ -245,8 +247,10 @@ static __device__ __noinline__ void interval_cells(double t, double L, double d,
   if (d >= 0.0) lb = L;
   else if (d1 <= 0.0) lb = L1;
   else {
-    const double x = (L1 - L + d * t - d1 * t1) / (d - d1);
-    lb = fmin(L + d * (x - t), fmin(L, L1));
+    // any x gives min(left tangent, right tangent) <= the minimum of their maximum, so an
+    // approximate intersection is still a valid lower bound
+    const double x = (L1 - L + d * t - d1 * t1) * rcp_1nt(d - d1);
+    lb = fmin(fmin(L + d * (x - t), L1 + d1 * (x - t1)), fmin(L, L1));
   }
   const bool keep = (lane < 31) && !(lb > thr);   // NaN keeps
   const unsigned mk = __ballot_sync(0xffffffffu, keep);
