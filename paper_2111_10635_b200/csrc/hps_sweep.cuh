@@ -206,8 +206,10 @@ __device__ __forceinline__ double cand_tau2(const WarpSmem<MAXS>& w, const Sweep
 template <int MAXS>
 __device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int S, double bo,
                                         double C, double tau, double& L, double& dL) {
+  // 16 grid points per level: lanes p and p + 16 share point p and split its stages (r even /
+  // odd), combined with one butterfly step
   double P = 0.0, dP = 0.0;
-  for (int r = 0; r < S; r++) {
+  for (int r = (threadIdx.x >> 4) & 1; r < S; r += 2) {
     const double km = (double)sw.kmi[r];
     double v = km * tau, dv = km;
     if (sw.kma[r] != sw.kmi[r]) {
@@ -230,12 +232,16 @@ __device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MA
     P += sw.pr[r] * v;
     dP += sw.pr[r] * dv;
   }
+  P += __shfl_xor_sync(0xffffffffu, P, 16);
+  dP += __shfl_xor_sync(0xffffffffu, dP, 16);
   L = C * P;
   dL = C * dP;
 }
 
-// One level of the interval search: lane j holds (t, L, dL) at grid point j of [ta, tb] (lane
-// 31 = tb). On each cell, convexity bounds L from below by max(tangent at the left end, tangent
+constexpr int kGrid = 16;   // grid points per level of the interval search
+
+// One level of the interval search: lane j < 16 holds (t, L, dL) at grid point j of [ta, tb]
+// (point 15 = tb). On each cell, convexity bounds L from below by max(tangent at the left end, tangent
 // at the right end); [ta, tb] shrinks to the cells whose bound does not exceed thr (ta > tb when
 // none does).
 static __device__ __noinline__ void interval_cells(double t, double L, double d, double thr, double& ta, double& tb) {
@@ -252,7 +258,7 @@ static __device__ __noinline__ void interval_cells(double t, double L, double d,
     const double x = (L1 - L + d * t - d1 * t1) * rcp_1nt(d - d1);
     lb = fmin(fmin(L + d * (x - t), L1 + d1 * (x - t1)), fmin(L, L1));
   }
-  const bool keep = (lane < 31) && !(lb > thr);   // NaN keeps
+  const bool keep = (lane < kGrid - 1) && !(lb > thr);   // NaN keeps
   const unsigned mk = __ballot_sync(0xffffffffu, keep);
   if (!mk) { ta = 1.0; tb = 0.0; return; }
   const int f = __ffs(mk) - 1, l = 31 - __clz(mk);
@@ -263,8 +269,8 @@ static __device__ __noinline__ void interval_cells(double t, double L, double d,
 
 template <int MAXS>
 __device__ __forceinline__ double grid_point(double ta, double tb) {
-  const int lane = threadIdx.x & 31;
-  return (lane == 31) ? tb : ta + (tb - ta) * (double)lane / 31.0;
+  const int p = threadIdx.x & (kGrid - 1);   // lanes p and p + 16 hold the same point
+  return (p == kGrid - 1) ? tb : ta + (tb - ta) * (double)p * (1.0 / (kGrid - 1));
 }
 
 // tie buffer overflow (rare): the largest tau of the restricted list whose exact cost is <= lim
