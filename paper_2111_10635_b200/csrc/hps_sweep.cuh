@@ -196,6 +196,14 @@ __device__ __forceinline__ double cand_tau2(const WarpSmem<MAXS>& w, const Sweep
   return __ldg(&w.row[sp][m - 1].et);
 }
 
+#ifndef HPS_GRID
+#define HPS_GRID 16
+#endif
+constexpr int kGrid = HPS_GRID;   // grid points per level of the interval search (power of 2)
+#ifndef HPS_GRID_LEVELS
+#define HPS_GRID_LEVELS 2
+#endif
+
 // Continuous lower bound of the cost of every certified breakpoint candidate tau:
 //   L(tau) = (work/batch) tau sum_r pr_r max(kmin_r, q_r(tau)(1 - 1e-8) - 1e-9),
 // q_r = max over sides of frac / (tau bo/work - (1 - frac)): count_r(tau) = ceil(max(1, q) - 1e-9)
@@ -206,10 +214,10 @@ __device__ __forceinline__ double cand_tau2(const WarpSmem<MAXS>& w, const Sweep
 template <int MAXS>
 __device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int S, double bo,
                                         double C, double tau, double& L, double& dL) {
-  // 16 grid points per level: lanes p and p + 16 share point p and split its stages (r even /
-  // odd), combined with one butterfly step
+  // kGrid points per level: lanes p, p + kGrid, ... share point p and split its stages,
+  // combined by butterfly steps
   double P = 0.0, dP = 0.0;
-  for (int r = (threadIdx.x >> 4) & 1; r < S; r += 2) {
+  for (int r = (threadIdx.x & 31) / kGrid; r < S; r += 32 / kGrid) {
     const double km = (double)sw.kmi[r];
     double v = km * tau, dv = km;
     if (sw.kma[r] != sw.kmi[r]) {
@@ -232,13 +240,14 @@ __device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MA
     P += sw.pr[r] * v;
     dP += sw.pr[r] * dv;
   }
-  P += __shfl_xor_sync(0xffffffffu, P, 16);
-  dP += __shfl_xor_sync(0xffffffffu, dP, 16);
+  for (int o = kGrid; o < 32; o <<= 1) {
+    P += __shfl_xor_sync(0xffffffffu, P, o);
+    dP += __shfl_xor_sync(0xffffffffu, dP, o);
+  }
   L = C * P;
   dL = C * dP;
 }
 
-constexpr int kGrid = 16;   // grid points per level of the interval search
 
 // One level of the interval search: lane j < 16 holds (t, L, dL) at grid point j of [ta, tb]
 // (point 15 = tb). On each cell, convexity bounds L from below by max(tangent at the left end, tangent
@@ -269,7 +278,7 @@ static __device__ __noinline__ void interval_cells(double t, double L, double d,
 
 template <int MAXS>
 __device__ __forceinline__ double grid_point(double ta, double tb) {
-  const int p = threadIdx.x & (kGrid - 1);   // lanes p and p + 16 hold the same point
+  const int p = threadIdx.x & (kGrid - 1);   // lanes p, p + kGrid, ... hold the same point
   return (p == kGrid - 1) ? tb : ta + (tb - ta) * (double)p * (1.0 / (kGrid - 1));
 }
 
@@ -401,7 +410,8 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
   if (grid && ub < inf) {
     const double thr = (ub + 1e-15) * (1.0 + 1e-7);
     interval_cells(g_t, g_L, g_d, thr, ta, tbh);
-    if (ta <= tbh) {
+#pragma unroll 1
+    for (int lvl = 1; lvl < HPS_GRID_LEVELS && ta <= tbh; lvl++) {
       const double t1 = grid_point<MAXS>(ta, tbh);
       double L1, d1;
       lb_cont<MAXS>(w, sw, S, c.bo, C, t1, L1, d1);
