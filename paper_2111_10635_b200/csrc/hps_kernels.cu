@@ -996,6 +996,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
       sw.kma[r] = hi;
       sw.etp[r] = (lo == hi) ? __ldg(&w.row[r][lo - 1].et) : 0.0;
       sw.dom[r] = pp.dom[r];
+      est_setup<MAXS>(w, sw, r);
       sw.lead[r] = pp.lead[r];
       sw.alo[r] = pp.alo[r];
       sw.an[r] = pp.an[r];

@@ -41,6 +41,7 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
 
   int32_t top[kTop > 0 ? kTop : 1]; // unpinned stages with the largest price-weighted count span (-1: none)
   int32_t dom[MAXS]; // side_dominance over [tau_lo, tau_hi]: 1 oct, 2 odt, 0 both
+  float est[MAXS][6];  // count_est seed constants (est_setup)
   int8_t lead[MAXS]; // class leader of stage r (stages of one class have identical counts)
   int32_t gex[MAXS]; // leader r: count_r(et_r(m)) == m for m <= gex[r] (tb.gex), else 0
   double q[64];      // survivors of the lower-bound filter, evaluated 32 at a time
@@ -49,20 +50,31 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
 
 // FP32 estimate of count(tau) of unpinned stage r, clamped to [kmin, kmax]. Only a seed: the
 // threshold table confirms or corrects it (count_verify), so it never affects a result.
+// per-stage FP32 seed constants {rb, 1 - frac, frac} of both sides; a side that cannot decide the
+// count (work 0, frac 0, or dominated per side_dominance) is {0, -1, 0} and contributes q = 0
 template <int MAXS>
-__device__ __forceinline__ int count_est(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r, float tf) {
+__device__ __forceinline__ void est_setup(const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int r) {
   const StageEntry& s = w.st[r];
   const int dom = sw.dom[r];
-  float q = 1.0f;
 #pragma unroll
   for (int side = 0; side < 2; side++) {
-    if (dom == 2 - side) continue;
     const float rb = side ? s.f_rbd : s.f_rbo;
     const float frac = side ? s.f_beta : s.f_alpha;
-    if (rb == 0.0f || frac == 0.0f) continue;
-    const float h = tf * rb - (side ? s.f_omb : s.f_oma);
-    q = (h > 0.0f) ? fmaxf(q, frac * rcp_approx_f32(h)) : 3.0e38f;
+    const bool on = (dom != 2 - side) && rb != 0.0f && frac != 0.0f;
+    sw.est[r][3 * side + 0] = on ? rb : 0.0f;
+    sw.est[r][3 * side + 1] = on ? (side ? s.f_omb : s.f_oma) : -1.0f;
+    sw.est[r][3 * side + 2] = on ? frac : 0.0f;
   }
+}
+
+// FP32 estimate of count(tau) of unpinned stage r, clamped to [kmin, kmax]. Only a seed: the
+// threshold table confirms or corrects it (count_verify), so it never affects a result.
+template <int MAXS>
+__device__ __forceinline__ int count_est(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r, float tf) {
+  const float* e = sw.est[r];
+  const float q0 = e[2] * rcp_approx_f32(tf * e[0] - e[1]);
+  const float q1 = e[5] * rcp_approx_f32(tf * e[3] - e[4]);
+  const float q = fmaxf(1.0f, fmaxf(q0, q1));   // (NaN operands are ignored)
   const int lo = sw.kmi[r], hi = sw.kma[r];
   const int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
   return min(max(k, lo), hi);
@@ -326,6 +338,7 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
     sw.kma[r] = (int)w.kmax[r];
     sw.etp[r] = pinned ? w.row[r][(int)w.kmin[r] - 1].et : 0.0;
     sw.dom[r] = pinned ? 0 : side_dominance(w.st[r], tau_lo, tau_hi, c.bo);
+    est_setup<MAXS>(w, sw, r);
     int ld = 0;  // first stage of r's class
     while (w.cls[ld] != w.cls[r]) ld++;
     sw.lead[r] = (int8_t)ld;
