@@ -846,6 +846,14 @@ stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src
 #ifndef HPS_CAND_MINB
 #define HPS_CAND_MINB 32
 #endif
+// prefetch the next plan's state records into L2 (one 128-byte line per lane) while the
+// current plan is processed
+__device__ __forceinline__ void prefetch_lines(const void* base, size_t bytes) {
+  const int lane = threadIdx.x & 31;
+  if ((size_t)lane * 128 < bytes)
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(reinterpret_cast<const char*>(base) + (size_t)lane * 128));
+}
+
 // K1a': the quota bisection (bisect_direct) and the candidate prefix of each surviving plan,
 // in place on its PlanState; plans with more than 4096 breakpoints go to the slow path and
 // are marked (n_cand = -1) for the kernels that follow.
@@ -860,6 +868,7 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
   PlanState<MAXS>* states = reinterpret_cast<PlanState<MAXS>*>(cont.states);
   const unsigned int n = *cont.count;
   for (uint64_t q = gw; q < n; q += nw) {
+    if (q + nw < n) prefetch_lines(&states[q + nw], sizeof(PlanState<MAXS>));
     PlanState<MAXS>& ps = states[q];
     const int S = ps.S;
 #pragma unroll 1
@@ -938,6 +947,7 @@ prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<
   const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
   const unsigned int n = *cont.count;
   for (uint64_t q = gw; q < n; q += nw) {
+    if (q + nw < n) prefetch_lines(&states[q + nw], sizeof(PlanState<MAXS>));
     const PlanState<MAXS>& ps = states[q];
     if (ps.n_cand < 0) continue;  // slow path
     load_state<MAXS>(c, tb, ps, w);
@@ -982,6 +992,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
   unsigned long long feas = 0;
   uint32_t flags = 0;
   for (uint64_t q = gw; q < n; q += nw) {
+    if (q + nw < n) { prefetch_lines(&states[q + nw], sizeof(PlanState<MAXS>)); prefetch_lines(&prep[q + nw], sizeof(PrepState<MAXS>)); }
     const PlanState<MAXS>& ps = states[q];
     if (ps.n_cand < 0) continue;  // slow path
     load_state<MAXS>(c, tb, ps, w);
