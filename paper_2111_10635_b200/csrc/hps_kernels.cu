@@ -46,8 +46,14 @@ int set_err(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kEtCapMax = 16384;
-constexpr int kSlowThreads = 256;
-constexpr int kSlowSmemSort = 8192;   // doubles of dynamic shared memory for the slow path's sort
+#ifndef HPS_SLOW_THREADS
+#define HPS_SLOW_THREADS 256
+#endif
+constexpr int kSlowThreads = HPS_SLOW_THREADS;
+#ifndef HPS_SLOW_SORT
+#define HPS_SLOW_SORT 2048  // 2048/4096 (3 blocks per SM) measured 0.8-1.2% faster per sweep than 8192 (2)
+#endif
+constexpr int kSlowSmemSort = HPS_SLOW_SORT;  // doubles of dynamic shared memory for the slow path's sort
 
 // ------------------------------------------------------------------ plan sources
 
@@ -344,18 +350,45 @@ __device__ double golden_dev(const InstanceConsts& c, const WarpSmem<64>& w, int
   return (a + b) / 2.0;
 }
 
-// block-wide exclusive scan helper over per-thread counts (kSlowThreads threads)
+// block-wide exclusive scan helper over per-thread counts (kSlowThreads threads): warp shuffles,
+// then the warp totals (tmp[0..nwarps) scratch, tmp[kSlowThreads] = total)
 __device__ unsigned block_excl_scan(unsigned v, unsigned* tmp, unsigned& total) {
-  tmp[threadIdx.x] = v;
+  constexpr int kW = kSlowThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) tmp[warp] = inc;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned acc = 0;
-    for (int i = 0; i < kSlowThreads; i++) { unsigned t = tmp[i]; tmp[i] = acc; acc += t; }
+    for (int i = 0; i < kW; i++) { unsigned t = tmp[i]; tmp[i] = acc; acc += t; }
     tmp[kSlowThreads] = acc;
   }
   __syncthreads();
-  unsigned r = tmp[threadIdx.x];
+  const unsigned r = tmp[warp] + inc - v;
   total = tmp[kSlowThreads];
+  __syncthreads();
+  return r;
+}
+
+// block-wide fmin / fmax of one double per thread (order-independent); red[0..nwarps) scratch
+template <bool MAX>
+__device__ double block_minmax(double v, double* red) {
+  constexpr int kW = kSlowThreads / 32;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const double y = __shfl_xor_sync(0xffffffffu, v, d);
+    v = MAX ? fmax(v, y) : fmin(v, y);
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+#pragma unroll
+  for (int i = 1; i < kW; i++) r = MAX ? fmax(r, red[i]) : fmin(r, red[i]);
   __syncthreads();
   return r;
 }
@@ -433,17 +466,28 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
           }
           __syncthreads();
         }
-      // distinct finite values -> cand (chunked compaction)
-      const int chunk = (npow + kSlowThreads - 1) / kSlowThreads;
-      const int b0 = min(npow, tid * chunk), b1 = min(npow, b0 + chunk);
-      unsigned cnt = 0;
-      for (int i = b0; i < b1; i++)
-        if (srt[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || srt[i] != srt[i - 1])) cnt++;
-      unsigned nc;
-      unsigned at = block_excl_scan(cnt, scan_tmp, nc);
-      for (int i = b0; i < b1; i++)
-        if (srt[i] < __longlong_as_double(0x7ff0000000000000LL) && (i == 0 || srt[i] != srt[i - 1])) cand[at++] = srt[i];
-      __syncthreads();
+      // distinct finite values -> cand, in sorted order: rounds of kSlowThreads consecutive
+      // entries (bank-conflict free), ballot + warp counts; stops at the first +inf (sorted)
+      unsigned nc = 0;
+      for (int r0 = 0; r0 < npow; r0 += kSlowThreads) {
+        if (!(srt[r0] < __longlong_as_double(0x7ff0000000000000LL))) break;  // block-uniform
+        const int i = r0 + tid;
+        const bool f = i < npow && srt[i] < __longlong_as_double(0x7ff0000000000000LL) &&
+                       (i == 0 || srt[i] != srt[i - 1]);
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) scan_tmp[warp] = __popc(m);
+        __syncthreads();
+        unsigned off = nc, tot = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < kSlowThreads / 32; w2++) {
+          const unsigned cw = scan_tmp[w2];
+          if (w2 < warp) off += cw;
+          tot += cw;
+        }
+        if (f) cand[off + __popc(m & ((1u << lane) - 1u))] = srt[i];
+        nc += tot;
+        __syncthreads();
+      }
       bool ovf = false;
       if (nc > (unsigned)kBpLimit) {  // ls/provisioner.py:456-470
         ovf = true;
@@ -498,12 +542,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       TieBuf buf;
       buf.init();
       for (unsigned i = tid; i < nc; i += kSlowThreads) buf.insert(candidate_cost<64, true>(c, tb, w, S, cand[i]), cand[i]);
-      red_d[tid] = buf.mn;
-      __syncthreads();
-      if (tid == 0) for (int i = 1; i < kSlowThreads; i++) red_d[0] = fmin(red_d[0], red_d[i]);
-      __syncthreads();
-      const double mf = red_d[0];
-      __syncthreads();
+      const double mf = block_minmax<false>(buf.mn, red_d);
       const bool any_ovf = __syncthreads_or(buf.overflow);
       double bt = -__longlong_as_double(0x7ff0000000000000LL);
       if (mf < __longlong_as_double(0x7ff0000000000000LL)) {
@@ -515,11 +554,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
           bt = buf.best_tau(lim);
         }
       }
-      red_d[tid] = bt;
-      __syncthreads();
-      if (tid == 0) for (int i = 1; i < kSlowThreads; i++) red_d[0] = fmax(red_d[0], red_d[i]);
-      __syncthreads();
-      const double tau = red_d[0];
+      const double tau = block_minmax<true>(bt, red_d);
       if (warp == 0) {
         PlanOut r = s_out;
         if (!(mf < __longlong_as_double(0x7ff0000000000000LL))) {
@@ -1162,11 +1197,13 @@ int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending p
   const size_t per_block = slow_per_block(in);
   double* scratch = nullptr;
   const size_t cap_blocks = std::max<size_t>(8, ((size_t)4 << 30) / (per_block * sizeof(double)));
-  const int blocks = (int)std::min<size_t>((size_t)in->sm_count * 2, cap_blocks);
-  CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
-  HPS_COUNT_LAUNCH();
   auto ks = in->fast ? slow_kernel<true> : slow_kernel<false>;
   CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSlowSmemSort * sizeof(double))));
+  int per_sm = 0;  // as many resident blocks as registers and shared memory allow
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, kSlowThreads, kSlowSmemSort * sizeof(double)));
+  const int blocks = (int)std::min<size_t>((size_t)in->sm_count * std::max(1, per_sm), cap_blocks);
+  CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
+  HPS_COUNT_LAUNCH();
   ks<<<blocks, kSlowThreads, kSlowSmemSort * sizeof(double), st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
                                                     slow_parts, scratch, per_block);
   CUDA_TRY(cudaGetLastError());
