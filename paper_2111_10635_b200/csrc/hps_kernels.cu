@@ -396,7 +396,10 @@ __device__ double block_minmax(double v, double* red) {
 // FAST: quotas within the threshold tables (HpsInstance::fast): the exact table-driven bisection
 // and final phase; otherwise the literal arithmetic of both.
 template <bool FAST>
-__global__ void __launch_bounds__(kSlowThreads)
+#ifndef HPS_SLOW_MINB
+#define HPS_SLOW_MINB 4  // 64 registers, 4 resident blocks per SM: -2.5% per cfg3 sweep vs 80 registers
+#endif
+__global__ void __launch_bounds__(kSlowThreads, HPS_SLOW_MINB)
 slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, Outputs o,
             Pending pend, int argmin_mode, int feasible_only, KeyPart* slow_parts,
             double* scratch, size_t per_block) {
