@@ -37,7 +37,7 @@ UNIT = "plans/s"
 # reference-algorithm FP64 operations per plan on cfg3 (24*E[S*C] + 9*N_bp +
 # 13*61*S + 4*C + 88*L + 60*S with the measured means E[S*C]=7718, N_bp=697, S=11, C=689)
 W_REF_OPS = 205_052
-TRAFFIC_BYTES_PER_PLAN = 1839  # ncu dram__bytes_{read,write}.sum over a cfg3 sweep / plans (v34)
+TRAFFIC_BYTES_PER_PLAN = 2098  # ncu dram__bytes_{read,write}.sum over a cfg3 sweep / plans (v36)
 
 
 def parse():
@@ -373,7 +373,7 @@ def run_ours(args):
                                  f"({W_REF_OPS}, SURVEY.md §8(d)); peak = DFMA probe measured in "
                                  "this run (MEASURED_PEAKS.json has no FP64); traffic = DRAM "
                                  f"bytes per step at {TRAFFIC_BYTES_PER_PLAN} B/plan from the ncu "
-                                 "launch list (profiles/r1_launches_bench_v34_summary.txt): "
+                                 "launch list (profiles/r1_launches_bench_v36_summary.txt): "
                                  "the split kernels' per-plan state round trips, ~1.4% of HBM "
                                  "bandwidth at this rate"},
             "clocks": clocks.summary(),

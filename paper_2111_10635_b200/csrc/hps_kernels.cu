@@ -397,7 +397,7 @@ __device__ double block_minmax(double v, double* red) {
 // and final phase; otherwise the literal arithmetic of both.
 template <bool FAST>
 #ifndef HPS_SLOW_MINB
-#define HPS_SLOW_MINB 4  // 64 registers, 4 resident blocks per SM: -2.5% per cfg3 sweep vs 80 registers
+#define HPS_SLOW_MINB 6  // 40 registers, 6 resident blocks per SM: 653 -> 629 ms per cfg3 sweep (4: 633 ms)
 #endif
 __global__ void __launch_bounds__(kSlowThreads, HPS_SLOW_MINB)
 slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src, Outputs o,
