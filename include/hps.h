@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define HPS_ABI_VERSION 1
+#define HPS_ABI_VERSION 2
 #define HPS_MAX_LAYERS 64
 #define HPS_MAX_TYPES 16
 #define HPS_BREAKPOINT_LIMIT 4096 /* ls/provisioner.py:49 */
@@ -101,8 +101,27 @@ typedef struct HpsPlanResults {
   double* gap;         /* InfeasibleError.gap (0 when feasible) */
   int32_t* ps;         /* ProvisioningPlan.ps_cores */
   int32_t* num_stages; /* len(build_stages(plan)) */
-  int32_t* k;          /* ProvisioningPlan.per_stage_k */
+  int32_t* k;          /* ProvisioningPlan.per_stage_k; also the rejected counts of an
+                          HPS_ST_PS_QUOTA plan (the PS check runs on final counts) */
 } HpsPlanResults;
+
+/* Details of an infeasible plan: the values the reference's InfeasibleError text names
+ * (ls/provisioner.py:98-101 min_k1, :164-174 _floor_count at tau_hi, :407-411 serial floor,
+ * :421-425 quota at tau_hi, :508-511 PS cores). Filled per status; other fields are 0. */
+typedef struct HpsExplain {
+  int32_t status;       /* HPS_ST_* code the fields describe (the status passed in, masked) */
+  int32_t stage;        /* MIN_K1: 0; SERIAL: the (first) stage with the largest serial time;
+                           FLOOR_TAU_HI: the first stage whose _floor_count raises */
+  int32_t side;         /* MIN_K1 / FLOOR_TAU_HI: 0 computation, 1 communication */
+  int32_t serial_side;  /* FLOOR_TAU_HI: 1 when that side has frac == 0 ("serial ... time") */
+  int32_t type;         /* QUOTA_TAU_HI: first offending type id; PS_QUOTA: cheapest CPU type */
+  int32_t pad;
+  uint64_t units_hi;    /* QUOTA_TAU_HI: that type's units at tau_hi (Python int, 128 bits); */
+  uint64_t units_lo;    /* PS_QUOTA: the CPU type's units including the PS cores */
+  int64_t ps;           /* PS_QUOTA: parameter-server cores */
+  double serial;        /* SERIAL: _serial_floor(stages) */
+  double tau_hi;        /* SERIAL: tau_hi */
+} HpsExplain;
 
 /* Argmin key over a set of plans: (cost, lexicographic rank of the assignment). The rank is
  * the base-T number with layer 0 most significant (= itertools.product index), 128 bits. */
@@ -136,6 +155,11 @@ int hps_stage_table(HpsInstance* inst, int32_t type_id, int32_t first, int32_t l
 /* Score n plans (u8 [n][L] in device memory, ids in [0,T)). Stream-ordered. */
 int hps_score_plans(HpsInstance* inst, const uint8_t* d_plans, int64_t n,
                     const HpsPlanResults* d_out, void* stream);
+
+/* Message details of scored plans: d_status / d_k are hps_score_plans outputs for the same
+ * plans (k is read for HPS_ST_PS_QUOTA only). One HpsExplain per plan to d_out (device). */
+int hps_explain(HpsInstance* inst, const uint8_t* d_plans, const uint8_t* d_status,
+                const int32_t* d_k, int64_t n, HpsExplain* d_out, void* stream);
 
 /* Brute force over enumeration indices [begin, end) (T^L must fit 64 bits). feasible_only=1
  * keeps only status-OK plans (ls/baselines.py:83-84); ties go to the smaller index

@@ -634,6 +634,7 @@ static void score_plan(const HpsInstanceDesc* d, const uint8_t* plan, Scratch* w
         if (st[s].type == ps_type) have += best_k[s];
       long long would = have + ps;
       if (would > d->quota[ps_type]) {
+        for (int s = 0; s < S; s++) r->k[s] = best_k[s];  /* the rejected final counts */
         r->status = HPS_ST_PS_QUOTA | (ovf ? HPS_ST_OVERFLOW_FLAG : 0);
         r->gap = clamp_gap((double)(would - d->quota[ps_type]) / (double)d->quota[ps_type]);
         r->cost = penalty_cost(d, r->gap);
@@ -688,7 +689,8 @@ static void* batch_worker(void* arg) {
     if (j->ncand) j->ncand[i] = r.ncand;
     if (j->k) {
       for (int s = 0; s < L; s++) j->k[(size_t)i * L + s] = s < r.num_stages ? r.k[s] : 0;
-      if (r.status & 0x7f) memset(j->k + (size_t)i * L, 0, sizeof(int32_t) * L);
+      if ((r.status & 0x7f) != HPS_ST_OK && (r.status & 0x7f) != HPS_ST_PS_QUOTA)
+        memset(j->k + (size_t)i * L, 0, sizeof(int32_t) * L);
     }
   }
   free(w.cand);
@@ -768,6 +770,96 @@ int hpso_enum_argmin(const HpsInstanceDesc* d, uint64_t begin, uint64_t end, int
     pthread_join(tid[t], NULL);
     *feasible += jobs[t].feasible;
     /* shards are in index order, so strict < keeps the earliest index on ties */
+    if (jobs[t].best < *best_cost) { *best_cost = jobs[t].best; *best_idx = jobs[t].best_idx; }
+  }
+  return 0;
+}
+
+/* ---- full-sweep digest (test infrastructure: pins every plan of a sweep, not only the winner)
+ * Per plan the outputs the device writes (cost bits, status byte, gap bits, PS cores, stage
+ * count, per-stage counts; k and ps are 0 unless status == OK) are chained through splitmix64
+ * together with the enumeration index; the digest is the wrapping 64-bit SUM over plans, so it
+ * does not depend on the order in which shards or threads visit the plans. tests/sweep_digest.py
+ * computes the same function from device outputs. */
+static uint64_t smix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+uint64_t hpso_plan_hash(uint64_t idx, double cost, int status, double gap, int ps, int S,
+                        const int32_t* k, int L) {
+  uint64_t cb, gb;
+  memcpy(&cb, &cost, 8);
+  memcpy(&gb, &gap, 8);
+  const int ok = (status & 0x7f) == HPS_ST_OK;
+  uint64_t h = smix(idx);
+  h = smix(h ^ cb);
+  h = smix(h ^ gb);
+  h = smix(h ^ ((uint64_t)(status & 0xff) | ((uint64_t)(ok ? ps : 0) << 8) | ((uint64_t)S << 40)));
+  for (int s = 0; s < L; s++) h = smix(h ^ (uint64_t)(uint32_t)((ok && s < S) ? k[s] : 0) ^ ((uint64_t)s << 32));
+  return h;
+}
+
+typedef struct {
+  const HpsInstanceDesc* d;
+  uint64_t lo, hi;
+  double best;
+  uint64_t best_idx, feasible, digest;
+  uint64_t by_status[16];
+  uint64_t overflow;
+} DigestJob;
+
+static void* digest_worker(void* arg) {
+  DigestJob* j = (DigestJob*)arg;
+  Scratch w = {0};
+  HpsoResult r;
+  uint8_t plan[MAXL];
+  const int L = j->d->num_layers;
+  j->best = INFINITY;
+  j->best_idx = UINT64_MAX;
+  for (uint64_t i = j->lo; i < j->hi; i++) {
+    decode(i, j->d->num_types, L, plan);
+    score_plan(j->d, plan, &w, &r);
+    const int code = r.status & 0x7f;
+    j->by_status[code & 15]++;
+    if (r.status & HPS_ST_OVERFLOW_FLAG) j->overflow++;
+    j->digest += hpso_plan_hash(i, r.cost, r.status, r.gap, r.ps, r.num_stages, r.k, L);
+    if (code != HPS_ST_OK) continue;
+    j->feasible++;
+    if (r.cost < j->best) { j->best = r.cost; j->best_idx = i; }
+  }
+  free(w.cand);
+  free(w.mat);
+  return NULL;
+}
+
+/* brute force over [begin, end) plus the sweep digest and per-status plan counts
+ * (out18: feasible, digest, overflow count, by_status[0..15)) */
+int hpso_enum_digest(const HpsInstanceDesc* d, uint64_t begin, uint64_t end, int threads,
+                     double* best_cost, uint64_t* best_idx, uint64_t* out18) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t tid[256];
+  static DigestJob jobs[256];
+  const uint64_t n = end - begin;
+  for (int t = 0; t < threads; t++) {
+    memset(&jobs[t], 0, sizeof(DigestJob));
+    jobs[t].d = d;
+    jobs[t].lo = begin + (uint64_t)((u128)n * t / threads);
+    jobs[t].hi = begin + (uint64_t)((u128)n * (t + 1) / threads);
+    pthread_create(&tid[t], NULL, digest_worker, &jobs[t]);
+  }
+  *best_cost = INFINITY;
+  *best_idx = UINT64_MAX;
+  memset(out18, 0, 18 * sizeof(uint64_t));
+  for (int t = 0; t < threads; t++) {
+    pthread_join(tid[t], NULL);
+    out18[0] += jobs[t].feasible;
+    out18[1] += jobs[t].digest;
+    out18[2] += jobs[t].overflow;
+    for (int c = 0; c < 15; c++) out18[3 + c] += jobs[t].by_status[c];
     if (jobs[t].best < *best_cost) { *best_cost = jobs[t].best; *best_idx = jobs[t].best_idx; }
   }
   return 0;

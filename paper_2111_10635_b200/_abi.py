@@ -65,7 +65,15 @@ class HpsPcg64(C.Structure):
                 ("inc_hi", C.c_uint64), ("inc_lo", C.c_uint64)]
 
 
+class HpsExplain(C.Structure):
+    _fields_ = [("status", C.c_int32), ("stage", C.c_int32), ("side", C.c_int32),
+                ("serial_side", C.c_int32), ("type", C.c_int32), ("pad", C.c_int32),
+                ("units_hi", C.c_uint64), ("units_lo", C.c_uint64), ("ps", C.c_int64),
+                ("serial", C.c_double), ("tau_hi", C.c_double)]
+
+
 ARGMIN_NBYTES = C.sizeof(HpsArgmin)  # 48
+EXPLAIN_NBYTES = C.sizeof(HpsExplain)  # 64
 
 
 class StagedDesc:
@@ -160,6 +168,8 @@ _SIGNATURES = {
     "hps_score_plans_static": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                          C.c_void_p, C.c_void_p]),
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),
+    "hps_explain": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                              C.c_void_p, C.c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
@@ -181,7 +191,7 @@ def load_library(path: Path | None = None):
     for name, (res, args) in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype, fn.argtypes = res, args
-    if lib.hps_abi_version() != 1:
+    if lib.hps_abi_version() != 2:
         raise NativeUnavailableError("libhps.so ABI version mismatch")
     if path is None:
         _lib = lib

@@ -179,7 +179,8 @@ struct Outputs {  // mode 0 per-plan outputs (HpsPlanResults)
 struct Pending {
   unsigned long long* list;  // plan numbers that need the slow path
   unsigned int* count;
-  unsigned int cap;
+  unsigned int cap;          // == the plans of the launch it serves: every plan is pushed at most
+                             // once per super-chunk, so the list cannot overflow (run_super)
 };
 
 template <int MAXS>
@@ -187,6 +188,7 @@ __device__ __forceinline__ void write_plan(const InstanceConsts& c, const WarpSm
                                            const Outputs& o, uint64_t p, const PlanOut& r) {
   const int lane = threadIdx.x & 31;
   const bool ok = (r.status & 0x7f) == HPS_ST_OK;
+  const bool counts = ok || (r.status & 0x7f) == HPS_ST_PS_QUOTA;  // final counts exist
   if (lane == 0) {
     o.cost[p] = r.cost;
     o.status[p] = (uint8_t)r.status;
@@ -196,7 +198,7 @@ __device__ __forceinline__ void write_plan(const InstanceConsts& c, const WarpSm
   }
   if (o.k) {
     for (int s = lane; s < c.L; s += 32)
-      o.k[p * (uint64_t)c.L + s] = (ok && s < r.S) ? (int32_t)w.kres[s] : 0;
+      o.k[p * (uint64_t)c.L + s] = (counts && s < r.S) ? (int32_t)w.kres[s] : 0;
   }
 }
 
@@ -415,7 +417,13 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* raw = scratch + (size_t)blockIdx.x * per_block;  // [per_block/2] sort buffer
   double* cand = raw + per_block / 2;                       // distinct / kept candidates
-  const unsigned total = min(*pend.count, pend.cap);
+  const unsigned total = min(*pend.count, pend.cap);  // (count <= cap by construction)
+  Key acc;  // per-block argmin partial (thread 0), written once at the end
+  acc.cost = __longlong_as_double(0x7ff0000000000000LL);
+  acc.hi = acc.lo = ~0ull;
+  acc.status = 0;
+  unsigned long long acc_feas = 0;
+  uint32_t acc_flags = 0;
   for (unsigned item = blockIdx.x; item < total; item += gridDim.x) {
     const uint64_t p = pend.list[item];
     if (warp == 0) {
@@ -578,24 +586,19 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
         write_plan<64>(c, w, o, p, r);
       } else if (lane == 0) {
         const int code = r.status & 0x7f;
-        KeyPart kp;
-        kp.best.cost = __longlong_as_double(0x7ff0000000000000LL);
-        kp.best.hi = kp.best.lo = ~0ull;
-        kp.best.status = 0;
-        kp.evaluated = 0;
-        kp.feasible = (code == HPS_ST_OK);
-        kp.flags = (code == HPS_ST_NO_CPU_TYPE ? 1u : 0u) | (code == HPS_ST_INVALID ? 2u : 0u);
+        acc_feas += (code == HPS_ST_OK);
+        acc_flags |= (code == HPS_ST_NO_CPU_TYPE ? 1u : 0u) | (code == HPS_ST_INVALID ? 2u : 0u);
         const bool take = feasible_only ? (code == HPS_ST_OK) : (code != HPS_ST_NO_CPU_TYPE && code != HPS_ST_INVALID);
-        if (take) kp.best = Key{r.cost, (uint64_t)(s_rank >> 64), (uint64_t)s_rank, (uint32_t)r.status};
-        slow_parts[item] = kp;
+        const Key k{r.cost, (uint64_t)(s_rank >> 64), (uint64_t)s_rank, (uint32_t)r.status};
+        if (take && key_less(k, acc)) acc = k;
       }
     }
     __syncthreads();
   }
+  if (argmin_mode && tid == 0) slow_parts[blockIdx.x] = KeyPart{acc, 0ull, acc_feas, acc_flags};
 }
 
-__global__ void finish_argmin(const KeyPart* parts, int nparts, const KeyPart* slow_parts,
-                              const unsigned int* slow_count, unsigned int slow_cap,
+__global__ void finish_argmin(const KeyPart* parts, int nparts, const KeyPart* slow_parts, int nslow,
                               uint64_t evaluated, HpsArgmin* out) {
   __shared__ KeyPart red[256];
   KeyPart acc;
@@ -604,8 +607,7 @@ __global__ void finish_argmin(const KeyPart* parts, int nparts, const KeyPart* s
   acc.best.status = 0;
   acc.feasible = 0;
   acc.flags = 0;
-  const unsigned ns = min(*slow_count, slow_cap);
-  for (int i = threadIdx.x; i < nparts + (int)ns; i += blockDim.x) {
+  for (int i = threadIdx.x; i < nparts + nslow; i += blockDim.x) {
     const KeyPart& k = (i < nparts) ? parts[i] : slow_parts[i - nparts];
     if (key_less(k.best, acc.best)) acc.best = k.best;
     acc.feasible += k.feasible;
@@ -627,6 +629,24 @@ __global__ void finish_argmin(const KeyPart* parts, int nparts, const KeyPart* s
     out->status = acc.best.status;
     out->flags = acc.flags;
   }
+}
+
+// merge of per-super-chunk results (argmin_common): same total order, counts summed
+__global__ void merge_argmin(const HpsArgmin* keys, int n, uint64_t evaluated, HpsArgmin* out) {
+  if (threadIdx.x != 0) return;
+  HpsArgmin acc = keys[0];
+  for (int i = 1; i < n; i++) {
+    const HpsArgmin& k = keys[i];
+    const bool less = (k.cost != acc.cost) ? (k.cost < acc.cost)
+                      : (k.rank_hi != acc.rank_hi) ? (k.rank_hi < acc.rank_hi) : (k.rank_lo < acc.rank_lo);
+    const unsigned long long feas = acc.feasible + k.feasible;
+    const uint32_t flags = acc.flags | k.flags;
+    if (less) acc = k;
+    acc.feasible = feas;
+    acc.flags = flags;
+  }
+  acc.evaluated = evaluated;
+  *out = acc;
 }
 
 // ------------------------------------------------------------------ setup kernels
@@ -779,6 +799,8 @@ struct HpsInstance {
   int sm_count = 148;
   int grid_per_sm = 16;   // blocks per SM of the split kernels' grid (HPS_GRID_PER_SM)
   int carveout = -1;      // shared-memory carveout % for the split kernels (HPS_CARVEOUT)
+  int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
+  uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
 };
 
 namespace {
@@ -1195,16 +1217,28 @@ size_t slow_per_block(const HpsInstance* in) {
   return 2 * npow;  // doubles: sort buffer + candidate buffer
 }
 
+// resident slow-path blocks (occupancy API, cached) and the grid: one launch per super-chunk
+int slow_grid(HpsInstance* in, int& blocks) {
+  auto ks = in->fast ? slow_kernel<true> : slow_kernel<false>;
+  if (in->slow_per_sm < 0) {
+    CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSlowSmemSort * sizeof(double))));
+    int per_sm = 0;  // as many resident blocks as registers and shared memory allow
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, kSlowThreads, kSlowSmemSort * sizeof(double)));
+    in->slow_per_sm = std::max(1, per_sm);
+  }
+  const size_t per_block = slow_per_block(in);
+  const size_t cap_blocks = std::max<size_t>(8, ((size_t)4 << 30) / (per_block * sizeof(double)));
+  blocks = (int)std::min<size_t>((size_t)in->sm_count * in->slow_per_sm, cap_blocks);
+  return HPS_OK;
+}
+
 int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending pend, int argmin_mode,
              int feasible_only, KeyPart* slow_parts, cudaStream_t st) {
+  int blocks = 0;
+  if (int rc = slow_grid(in, blocks)) return rc;
   const size_t per_block = slow_per_block(in);
   double* scratch = nullptr;
-  const size_t cap_blocks = std::max<size_t>(8, ((size_t)4 << 30) / (per_block * sizeof(double)));
   auto ks = in->fast ? slow_kernel<true> : slow_kernel<false>;
-  CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSlowSmemSort * sizeof(double))));
-  int per_sm = 0;  // as many resident blocks as registers and shared memory allow
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, kSlowThreads, kSlowSmemSort * sizeof(double)));
-  const int blocks = (int)std::min<size_t>((size_t)in->sm_count * std::max(1, per_sm), cap_blocks);
   CUDA_TRY(cudaMallocAsync(&scratch, per_block * blocks * sizeof(double), st));
   HPS_COUNT_LAUNCH();
   ks<<<blocks, kSlowThreads, kSlowSmemSort * sizeof(double), st>>>(in->c, in->tb, src, o, pend, argmin_mode, feasible_only,
@@ -1212,6 +1246,15 @@ int run_slow(HpsInstance* in, const PlanSource& src, const Outputs& o, Pending p
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(scratch, st));
   return HPS_OK;
+}
+
+// plan source advanced by `off` plans (a super-chunk of the caller's range)
+PlanSource advance_source(const PlanSource& src, uint64_t off, int L) {
+  PlanSource s = src;
+  if (s.mode == 0) s.plans = src.plans + off * (uint64_t)L;
+  else if (s.mode == 1) s.begin = src.begin + off * src.stride;
+  else s.begin = src.begin + off;
+  return s;
 }
 
 void fill_random_source(HpsInstance* in, const HpsPcg64* g, uint64_t first, PlanSource& src) {
@@ -1232,48 +1275,54 @@ void fill_random_source(HpsInstance* in, const HpsPcg64* g, uint64_t first, Plan
   }
 }
 
-const uint64_t kSlowCap = 1u << 20;
-
-struct ArgminScratch {
-  KeyPart* parts;
-  KeyPart* slow_parts;
-  unsigned long long* list;
-  unsigned int* count;
-};
-
+// Argmin over plans [0, n) of src, in super-chunks of at most in->super_chunk plans: each runs the
+// warp kernels, then the slow path over that chunk's pending list (sized to the chunk, so no plan
+// is ever dropped), then the merge into one key per chunk; the chunk keys merge at the end.
 int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_only, HpsArgmin* d_best,
                   cudaStream_t st) {
   if (n == 0) {   // empty range: the identity key (cost +inf, nothing evaluated)
-    unsigned int* zero = nullptr;
-    CUDA_TRY(cudaMallocAsync(&zero, sizeof(unsigned int), st));
-    CUDA_TRY(cudaMemsetAsync(zero, 0, sizeof(unsigned int), st));
     HPS_COUNT_LAUNCH();
-    finish_argmin<<<1, 256, 0, st>>>(nullptr, 0, nullptr, zero, 0, 0, d_best);
+    finish_argmin<<<1, 256, 0, st>>>(nullptr, 0, nullptr, 0, 0, d_best);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaFreeAsync(zero, st));
     return HPS_OK;
   }
-  const int grid = grid_for(in, n);
+  const uint64_t sc = in->super_chunk;
+  const uint64_t nsc = (n + sc - 1) / sc;
+  const uint64_t n0 = std::min(n, sc);
+  const int grid = grid_for(in, n0);   // one grid for every chunk: every warp writes its partial
   const int nparts = grid * warps_per_block(in) * (in->fast ? 2 : 1);
-  const unsigned cap = (unsigned)std::min<uint64_t>(kSlowCap, std::max<uint64_t>(n, 1));
+  int nslow = 0;
+  if (int rc = slow_grid(in, nslow)) return rc;
+  const unsigned cap = (unsigned)n0;
   char* buf = nullptr;
-  const size_t bytes = sizeof(KeyPart) * (nparts + cap) + sizeof(unsigned long long) * cap + 64;
+  const size_t bytes = sizeof(KeyPart) * (nparts + nslow) + sizeof(HpsArgmin) * (nsc > 1 ? nsc : 0) +
+                       sizeof(unsigned long long) * cap + 64;
   CUDA_TRY(cudaMallocAsync(&buf, bytes, st));
   KeyPart* parts = reinterpret_cast<KeyPart*>(buf);
   KeyPart* slow_parts = parts + nparts;
-  unsigned long long* list = reinterpret_cast<unsigned long long*>(slow_parts + cap);
+  HpsArgmin* chunk_keys = reinterpret_cast<HpsArgmin*>(slow_parts + nslow);
+  unsigned long long* list = reinterpret_cast<unsigned long long*>(chunk_keys + (nsc > 1 ? nsc : 0));
   unsigned int* count = reinterpret_cast<unsigned int*>(list + cap);
-  CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
-  Pending pend{list, count, cap};
   Outputs o{};
-  int rc = in->fast ? dispatch_split<true>(in, src, n, o, pend, feasible_only, parts, grid, st)
-                    : dispatch_eval<true>(in, src, n, o, pend, feasible_only, parts, grid, st);
-  if (rc) return rc;
-  rc = run_slow(in, src, o, pend, 1, feasible_only, slow_parts, st);
-  if (rc) return rc;
-  HPS_COUNT_LAUNCH();
-  finish_argmin<<<1, 256, 0, st>>>(parts, nparts, slow_parts, count, cap, n, d_best);
-  CUDA_TRY(cudaGetLastError());
+  for (uint64_t i = 0; i < nsc; i++) {
+    const uint64_t s0 = i * sc, m = std::min(n, s0 + sc) - s0;
+    const PlanSource sub = advance_source(src, s0, in->c.L);
+    CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
+    Pending pend{list, count, (unsigned)m};
+    int rc = in->fast ? dispatch_split<true>(in, sub, m, o, pend, feasible_only, parts, grid, st)
+                      : dispatch_eval<true>(in, sub, m, o, pend, feasible_only, parts, grid, st);
+    if (rc) return rc;
+    rc = run_slow(in, sub, o, pend, 1, feasible_only, slow_parts, st);
+    if (rc) return rc;
+    HPS_COUNT_LAUNCH();
+    finish_argmin<<<1, 256, 0, st>>>(parts, nparts, slow_parts, nslow, m, nsc > 1 ? chunk_keys + i : d_best);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (nsc > 1) {
+    HPS_COUNT_LAUNCH();
+    merge_argmin<<<1, 32, 0, st>>>(chunk_keys, (int)nsc, n, d_best);
+    CUDA_TRY(cudaGetLastError());
+  }
   CUDA_TRY(cudaFreeAsync(buf, st));
   return HPS_OK;
 }
@@ -1299,8 +1348,13 @@ const char* hps_error_string(int code) {
 
 const char* hps_last_error(void) { return g_last_error.c_str(); }
 
+namespace {
+int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& d_raw);
+}
+
 int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   if (!d || !out) return set_err(HPS_E_INVALID_ARG, "null argument");
+  *out = nullptr;
   const int L = d->num_layers, T = d->num_types;
   if (L < 1 || L > kMaxL || T < 1 || T > kMaxT) return set_err(HPS_E_CONFIG, "L or T out of range");
   if (!(d->throughput_limit > 0) || d->profile_batch_size < 1 || d->batch_size < 1)
@@ -1310,9 +1364,26 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   if (ndev < 1) return set_err(HPS_E_CUDA, "no CUDA device");
   CUDA_TRY(cudaGetDevice(&dev));
   auto* in = new HpsInstance();
+  double* d_raw = nullptr;
+  const int rc = instance_build(d, in, dev, d_raw);
+  if (d_raw) cudaFree(d_raw);
+  if (rc != HPS_OK) {   // every partially created table is released (destroy tolerates nulls)
+    hps_instance_destroy(in);
+    return rc;
+  }
+  *out = in;
+  return HPS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& d_raw) {
+  const int L = d->num_layers, T = d->num_types;
   cudaDeviceGetAttribute(&in->sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (const char* e = getenv("HPS_GRID_PER_SM")) in->grid_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("HPS_CARVEOUT")) in->carveout = std::min(100, atoi(e));
+  if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -1356,7 +1427,6 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   in->fast = fast && (getenv("HPS_FORCE_LITERAL") == nullptr);
   // raw tables -> device
   const size_t tl = (size_t)T * L * sizeof(double);
-  double* d_raw = nullptr;
   CUDA_TRY(cudaMalloc(&d_raw, 4 * tl));
   CUDA_TRY(cudaMemcpy(d_raw, d->oct, tl, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy((char*)d_raw + tl, d->odt, tl, cudaMemcpyHostToDevice));
@@ -1392,6 +1462,7 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   }
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaFree(d_raw));
+  d_raw = nullptr;
   // ET-equivalence classes: group entries with bitwise-equal (oct, odt, alpha, beta)
   in->h_stages.resize(ne);
   CUDA_TRY(cudaMemcpy(in->h_stages.data(), in->d_stages, sizeof(StageEntry) * ne, cudaMemcpyDeviceToHost));
@@ -1408,9 +1479,11 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
   }
   CUDA_TRY(cudaMemcpy(in->d_cls, cls.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
   in->tb = DeviceTables{in->d_stages, in->d_stage0, in->d_te, in->d_cls, in->d_gex};
-  *out = in;
   return HPS_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int hps_instance_destroy(HpsInstance* in) {
   if (!in) return HPS_OK;
@@ -1441,19 +1514,27 @@ int hps_score_plans(HpsInstance* in, const uint8_t* d_plans, int64_t n, const Hp
   PlanSource src{};
   src.mode = 0;
   src.plans = d_plans;
-  Outputs o{r->cost, r->status, r->gap, r->ps, r->num_stages, r->k};
-  const unsigned cap = (unsigned)std::min<int64_t>(n, (int64_t)kSlowCap);
+  // super-chunks as in argmin_common: the pending list holds a whole chunk
+  const uint64_t sc = in->super_chunk;
+  const uint64_t cap = std::min<uint64_t>((uint64_t)n, sc);
   char* buf = nullptr;
   CUDA_TRY(cudaMallocAsync(&buf, sizeof(unsigned long long) * cap + 64, st));
   unsigned long long* list = reinterpret_cast<unsigned long long*>(buf);
   unsigned int* count = reinterpret_cast<unsigned int*>(list + cap);
-  CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
-  Pending pend{list, count, cap};
-  int rc = in->fast ? dispatch_split<false>(in, src, (uint64_t)n, o, pend, 0, nullptr, grid_for(in, n), st)
-                    : dispatch_eval<false>(in, src, (uint64_t)n, o, pend, 0, nullptr, grid_for(in, n), st);
-  if (rc) return rc;
-  rc = run_slow(in, src, o, pend, 0, 0, nullptr, st);
-  if (rc) return rc;
+  const int L = in->c.L;
+  for (uint64_t s0 = 0; s0 < (uint64_t)n; s0 += sc) {
+    const uint64_t m = std::min<uint64_t>((uint64_t)n, s0 + sc) - s0;
+    const PlanSource sub = advance_source(src, s0, L);
+    Outputs o{r->cost + s0, r->status + s0, r->gap ? r->gap + s0 : nullptr, r->ps ? r->ps + s0 : nullptr,
+              r->num_stages ? r->num_stages + s0 : nullptr, r->k ? r->k + s0 * (uint64_t)L : nullptr};
+    CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned int), st));
+    Pending pend{list, count, (unsigned)m};
+    int rc = in->fast ? dispatch_split<false>(in, sub, m, o, pend, 0, nullptr, grid_for(in, m), st)
+                      : dispatch_eval<false>(in, sub, m, o, pend, 0, nullptr, grid_for(in, m), st);
+    if (rc) return rc;
+    rc = run_slow(in, sub, o, pend, 0, 0, nullptr, st);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaFreeAsync(buf, st));
   return HPS_OK;
 }
@@ -1581,7 +1662,101 @@ __global__ void report_kernel(const InstanceConsts c, const DeviceTables tb, con
   cost[i] = ex * per_second;
   feasible[i] = (overall > c.limit) && quota_ok;
 }
+
+// InfeasibleError details (ls/provisioner.py:98-101, 164-174, 407-411, 421-425, 508-511), one
+// thread per plan: the fields the reference's message text names, recomputed from the stage
+// table for the status the scorer returned.
+__global__ void explain_kernel(const InstanceConsts c, const DeviceTables tb, const uint8_t* plans,
+                               const uint8_t* status, const int32_t* k, int64_t n, HpsExplain* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int L = c.L;
+  const uint8_t* pl = plans + i * L;
+  HpsExplain e;
+  memset(&e, 0, sizeof(e));
+  e.status = status[i] & 0x7f;
+  int ent[kMaxL];
+  int S = 0, last0 = L - 1;
+  for (int pos = 1, start = 0; pos <= L; pos++) {   // build_stages runs (ls/domain.py:293-296)
+    if (pos < L && pl[pos] == pl[start]) continue;
+    if (pl[start] >= c.T) { out[i] = e; return; }
+    if (S == 0) last0 = pos - 1;
+    ent[S++] = entry_index(c.P, pl[start], start, pos - 1);
+    start = pos;
+  }
+  const StageEntry& s0 = tb.stages[ent[0]];
+  const double tau_hi = tb.stage0[s0.type * L + last0].tau_hi;
+  if (e.status == HPS_ST_MIN_K1) {   // min_k1: computation side first (ls/provisioner.py:89-101)
+    const double budget = c.limit * c.bo;
+    e.side = (s0.oct != 0 && budget - (1.0 - s0.alpha) * s0.oct <= 0) ? 0 : 1;
+  } else if (e.status == HPS_ST_SERIAL) {   // max(stages, key=serial time): the first maximum
+    double best = -1.0;
+    for (int s = 0; s < S; s++) {
+      const double v = tb.stages[ent[s]].serial;
+      if (v > best) { best = v; e.stage = s; }
+    }
+    e.serial = 0.0;
+    for (int s = 0; s < S; s++) {   // _serial_floor: max(floor, ct side, dt side) per stage
+      const StageEntry& st = tb.stages[ent[s]];
+      e.serial = pmax(pmax(e.serial, st.c_oct * st.oma), st.c_odt * st.omb);
+    }
+    e.tau_hi = tau_hi;
+  } else if (e.status == HPS_ST_FLOOR_TAU_HI) {   // the first raising _floor_count at tau_hi
+    for (int s = 0; s < S; s++) {
+      const StageEntry& st = tb.stages[ent[s]];
+      bool raised = false;
+      for (int side = 0; side < 2 && !raised; side++) {
+        const double work = side ? st.odt : st.oct, frac = side ? st.beta : st.alpha;
+        if (work == 0) continue;
+        const double h = tau_hi * c.bo / work - (side ? st.omb : st.oma);
+        if (frac == 0.0 ? !(h >= 0) : (h <= 0)) {
+          raised = true;
+          e.stage = s; e.side = side; e.serial_side = (frac == 0.0);
+        }
+      }
+      if (raised) break;
+    }
+  } else if (e.status == HPS_ST_QUOTA_TAU_HI) {   // first type (ascending id) over its quota
+    u128 tot[kMaxT];
+    for (int t = 0; t < c.T; t++) tot[t] = 0;
+    for (int s = 0; s < S; s++) {
+      const StageEntry& st = tb.stages[ent[s]];
+      double r, g;
+      if (floor_count(st, tau_hi, c.bo, r, g)) tot[st.type] += dbl_to_u128(iceil(r));
+    }
+    for (int t = 0; t < c.T; t++)
+      if (tot[t] > (u128)c.quota[t]) {
+        e.type = t;
+        e.units_hi = (uint64_t)(tot[t] >> 64);
+        e.units_lo = (uint64_t)tot[t];
+        break;
+      }
+  } else if (e.status == HPS_ST_PS_QUOTA && k != nullptr && c.ps_type >= 0) {
+    long long accel = 0, have = 0;
+    for (int s = 0; s < S; s++) {
+      const int t = tb.stages[ent[s]].type;
+      const long long kk = k[i * L + s];
+      if (!c.is_cpu[t]) accel += kk;
+      if (t == c.ps_type) have += kk;
+    }
+    e.ps = (long long)ceil(c.ps_cores_per_gpu * (double)accel - 1e-9);
+    e.type = c.ps_type;
+    e.units_lo = (uint64_t)(have + e.ps);
+  }
+  out[i] = e;
+}
 }  // namespace
+
+extern "C" int hps_explain(HpsInstance* in, const uint8_t* d_plans, const uint8_t* d_status,
+                           const int32_t* d_k, int64_t n, HpsExplain* d_out, void* stream) {
+  if (!in || !d_plans || !d_status || !d_out || n < 0) return set_err(HPS_E_INVALID_ARG, "null argument");
+  if (n == 0) return HPS_OK;
+  HPS_COUNT_LAUNCH();
+  explain_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(in->c, in->tb, d_plans, d_status,
+                                                                                d_k, n, d_out);
+  CUDA_TRY(cudaGetLastError());
+  return HPS_OK;
+}
 
 std::atomic<unsigned long long> hps::g_launches{0};
 

@@ -154,6 +154,19 @@ class DeviceInstance:
                                                  _stream(stream)), "hps_random_plans")
         return out
 
+    def explain(self, plans, status, k=None, stream=None) -> list:
+        """InfeasibleError details of scored plans (hps_explain), as HpsExplain records."""
+        plans = plans.to(self.device).contiguous()
+        n = plans.shape[0]
+        out = torch.empty(n * _abi.EXPLAIN_NBYTES, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            _abi.check(self.lib.hps_explain(self.handle, _ptr(plans), _ptr(status.contiguous()),
+                                            _ptr(k.contiguous()) if k is not None else None, n,
+                                            _ptr(out), _stream(stream)), "hps_explain")
+        raw = bytes(out.cpu().numpy().tobytes())
+        m = _abi.EXPLAIN_NBYTES
+        return [_abi.HpsExplain.from_buffer_copy(raw[i * m:(i + 1) * m]) for i in range(n)]
+
     @staticmethod
     def read_argmin(buf) -> dict:
         return argmin_from_bytes(bytes(buf.cpu().numpy().tobytes()))

@@ -19,7 +19,6 @@ from __future__ import annotations
 import ctypes as C
 import json
 import math
-import time
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Callable
@@ -380,8 +379,11 @@ def train(graph, catalog, params0: PolicyParams, config: TrainerConfig, job,
     recorded = torch.empty((config.rounds, G, L), dtype=torch.uint8, device=dev) if record_plans else None
     draws = 0      # 64-bit draws consumed by Generator.random() so far
     halves = 0     # 32-bit halves consumed by Generator.integers() (warm-up rounds)
-    walls = []
-    t0 = time.perf_counter()
+    # round_wall_s[r-1]: seconds from the start of round 1 to the END of round r on the device
+    # timeline (CUDA events on the launching stream, read after the final synchronize)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    round_events = []
     for r in range(1, config.rounds + 1):
         dp.forward(config.temperature)
         if r <= config.warmup_rounds:
@@ -416,10 +418,13 @@ def train(graph, catalog, params0: PolicyParams, config: TrainerConfig, job,
             recorded[r - 1].copy_(plans)
         dp.reinforce(cost, status, plans, r, config.temperature, config.learning_rate,
                      config.baseline_rate, history, best_plan, best_where)
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        round_events.append(ev)
         if r % 16 == 0 or r == config.rounds:
             torch.cuda.current_stream().synchronize()
-        walls.append(time.perf_counter() - t0)
     torch.cuda.synchronize()
+    walls = [ev0.elapsed_time(ev) * 1e-3 for ev in round_events]
     _, flags = dp.state()
     if flags[0]:
         raise NumericError("non-finite activation in the policy forward pass")

@@ -84,6 +84,32 @@ def _totals(runs, k, ps, ps_type):
     return totals
 
 
+def infeasible_message(code: int, ex, catalog) -> str:
+    """The reference's InfeasibleError text for a device status and its hps_explain details
+    (ls/provisioner.py:98-101, 164-174, 407-411, 421-425, 473-477, 508-511)."""
+    label = ("computation", "communication")
+    if code == _abi.ST_MIN_K1:
+        return (f"stage {ex.stage} cannot reach the throughput limit at any count: serial "
+                f"{label[ex.side]} time exceeds the budget")
+    if code == _abi.ST_SERIAL:
+        return (f"stage {ex.stage} cannot reach the throughput limit at any count: its serial "
+                f"time {ex.serial:.6g}s is not below the budget {ex.tau_hi:.6g}s")
+    if code == _abi.ST_FLOOR_TAU_HI:
+        if ex.serial_side:
+            return f"stage {ex.stage}: serial {label[ex.side]} time exceeds the load-balance target"
+        return f"stage {ex.stage}: {label[ex.side]} cannot reach the load-balance target at any count"
+    if code == _abi.ST_QUOTA_TAU_HI:
+        rt = catalog.types[ex.type]
+        units = (ex.units_hi << 64) | ex.units_lo
+        return (f"no count within quota meets the throughput limit: type '{rt.name}' needs "
+                f"{units} units, quota is {rt.quota}")
+    if code == _abi.ST_PS_QUOTA:
+        rt = catalog.types[ex.type]
+        return (f"type '{rt.name}' needs {ex.units_lo} units including {ex.ps} parameter-server "
+                f"cores, quota is {rt.quota}")
+    return _MESSAGES.get(code, "infeasible plan")
+
+
 def raise_for_status(code: int, gap: float) -> None:
     if code == _abi.ST_OK:
         return
@@ -248,6 +274,11 @@ def _provisioning_from(out, plan, graph, catalog, params, inst, mode, cpu_per_gp
     if code == _abi.ST_STATIC_NONE:
         last = _static_violation(plan, catalog, params, inst, mode, cpu_per_gpu)
         raise InfeasibleError(_MESSAGES[code] + (f": {last}" if last else ""), gap=1.0)
+    if code not in (_abi.ST_OK, _abi.ST_INVALID, _abi.ST_NO_CPU_TYPE):
+        import torch
+        ex = inst.explain(torch.tensor([list(plan.assignment)], dtype=torch.uint8),
+                          out["status"], out["k"])[0]
+        raise InfeasibleError(infeasible_message(code, ex, catalog), gap=float(out["gap"][0].item()))
     raise_for_status(code, float(out["gap"][0].item()))
     S = int(out["num_stages"][0].item())
     k = tuple(int(x) for x in out["k"][0, :S].cpu().tolist())

@@ -1,11 +1,13 @@
 """Plan searchers on the device: brute_force and random_search (ls/baselines.py:63-87,230-282),
 plus greedy / genetic / heuristic_first_layer / homogeneous (ls/baselines.py:90-228).
 
-Both keep the reference's signature, cap, tie rules and returned ScoredPlan. The sweep is one
-fused kernel per GPU (in-kernel plan decode / generation + per-plan scoring + (cost, rank)
-argmin); with ``torch.distributed`` initialised the index range (or the random-plan stream) is
-split into contiguous per-rank shards and the per-rank winners meet in ONE all_gather of
-48-byte keys — the only exchange the path has.
+Both keep the reference's signature, cap, tie rules and returned ScoredPlan. The sweep runs on
+the device kernels (in-kernel plan decode / generation + per-plan scoring + (cost, rank)
+argmin); with ``torch.distributed`` initialised the enumeration is dealt round-robin (rank r
+sweeps indices r, r + W, r + 2W, ...: ``shard_strided``), the random-plan stream is split into
+contiguous slices (``shard_range``; the PCG64 stream is jumped in-kernel), and the per-rank
+winners meet in ONE all_gather of 48-byte keys — the only exchange the path has
+(SURVEY.md §8(e)).
 """
 
 from __future__ import annotations

@@ -56,6 +56,19 @@ def main_():
                     out.append({"instance": name, "limit": limit,
                                 "args": ["provision", "--plan", plan, "--mode", m, ps],
                                 "exit": r.exit_code, "stdout": r.stdout})
+        # infeasible plans: the InfeasibleError text on stderr, exit 2 (quota at tau_hi, PS
+        # cores over quota, serial floor)
+        q3 = [int(ch) for ch in "0111101111000001"]   # quota at tau_hi (plans_quota golden)
+        q6 = [int(ch) for ch in "1010011110101100"]   # PS cores over the CPU quota
+        for name, plan, extra in (("quota", [0] * 16, []), ("quota", q3, []),
+                                  ("quota", q6, []), ("quota", q6, ["--no-ps"]),
+                                  ("cfg2", [0, 1, 2, 0, 1, 2, 0, 1], [])):
+            limit = idx[name]["throughput_limit"]
+            p = Path(d) / "plan.json"
+            p.write_text(json.dumps({"assignment": plan}))
+            r = runner.invoke(main, ["provision"] + inst_args(name, limit) + ["--plan", str(p)] + extra)
+            out.append({"instance": name, "limit": limit, "args": ["provision", "--plan", plan] + extra,
+                        "exit": r.exit_code, "stdout": r.stdout})
     with gzip.open(HERE / "cli.json.gz", "wt") as f:
         json.dump(out, f)
     for o in out:

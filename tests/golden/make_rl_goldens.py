@@ -1,7 +1,7 @@
 """RL golden traces from the REFERENCE trainer (test infrastructure; run here only).
 
 For cfg1 (CTRDNN-4, T=2, G=64, R=200, seeds 0-2) and cfg4 (CTRDNN16, T=2, G=4096, first 12
-rounds, seed 0), record per round: RoundStats (mean_cost, best_cost, baseline, entropy as
+rounds, seed 0; `--cfg4-full`: all 200 rounds into rl_traces_cfg4_200.json.gz), record per round: RoundStats (mean_cost, best_cost, baseline, entropy as
 float.hex), a digest of the sampled plans (sha1 of the G x L action bytes), the number of
 infeasible plans, and the final parameters' checksum/norm; plus init parameters checksum.
 ls/policy/training.py:164-274 is run unmodified; sampling is observed by wrapping
@@ -66,6 +66,12 @@ def run(name, seed, rounds, G):
 
 
 def main():
+    if "--cfg4-full" in sys.argv:   # all 200 rounds of BASELINE cfg4 (~7 min on one core)
+        tr4 = run("cfg4", 0, 200, 4096)
+        print("cfg4 best", tr4["best_plan"], float.fromhex(tr4["best_cost"]), flush=True)
+        with gzip.open(HERE / "rl_traces_cfg4_200.json.gz", "wt") as f:
+            json.dump(tr4, f)
+        return
     out = []
     for seed in (0, 1, 2):
         out.append(run("cfg1", seed, 200, 64))

@@ -24,7 +24,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_abi.EXPORTED_SYMBOLS)
-    assert lib.hps_abi_version() == 1
+    assert lib.hps_abi_version() == 2
 
 
 def test_abi_struct_sizes_match_header():
