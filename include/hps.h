@@ -223,16 +223,21 @@ int hps_policy_params(HpsPolicy* policy, int32_t which, int32_t dir, double* hos
 /* K4: LSTM/Elman forward at the current parameters; probabilities [L][T] to d_probs (optional) */
 int hps_policy_forward(HpsPolicy* policy, double temperature, double* d_probs, void* stream);
 /* K3: n plans; plan g, layer t uses draw first_draw + g*L + t of the PCG64 stream, one
- * Generator.random() per Generator.choice(T, p) */
+ * Generator.random() per Generator.choice(T, p). first_draw = UINT64_MAX reads the policy's
+ * device counter (hps_policy_counter) instead. */
 int hps_policy_sample(HpsPolicy* policy, const HpsPcg64* gen, uint64_t first_draw, int64_t n,
                       uint8_t* d_plans, void* stream);
 /* K6+K5: one REINFORCE round from the G scored plans: best-ever, winsorising, standardising,
- * dlogits in trace order, BPTT, norm cap, update, moving-average baseline, RoundStats row */
+ * dlogits in trace order, BPTT, norm cap, update, moving-average baseline, RoundStats row.
+ * round = 0 takes the round number from the device counter. Every call advances the counter
+ * (round + 1, draws + G*L), so a captured round (CUDA graph) replays as the next round. */
 int hps_policy_reinforce(HpsPolicy* policy, const double* d_cost, const uint8_t* d_status,
                          const uint8_t* d_plans, int64_t num_plans, int32_t round,
                          double temperature, double learning_rate, double baseline_rate,
                          double* d_history, uint8_t* d_best_plan, long long* d_best_where,
                          void* stream);
+/* Set the device round counter: the next round's number (>= 1) and the draws consumed. */
+int hps_policy_counter(HpsPolicy* policy, uint64_t round, uint64_t draws, void* stream);
 /* {baseline, best cost, entropy} and {non-finite logits, non-finite params} flags */
 int hps_policy_state(HpsPolicy* policy, double* state3, int32_t* flags2);
 const char* hps_policy_last_error(void);

@@ -159,6 +159,7 @@ _SIGNATURES = {
                                        C.c_int32, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p]),
     "hps_policy_state": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hps_policy_counter": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
     "hps_policy_last_error": (C.c_char_p, []),
     "hps_probe_fp64": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "hps_stats_read": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),

@@ -38,27 +38,69 @@ int perr(int code, const std::string& m) {
 constexpr int kMaxH = 128;
 constexpr int kMaxD = 160;
 
-// numpy pairwise_sum over a strided double array (loops_utils.h.src), n >= 0
-__device__ double np_pairwise(const double* a, long n, long stride) {
-  // iterative restatement of the recursion: split points as numpy's pw(a, n)
+// numpy pairwise_sum (loops_utils.h.src): a block of n <= 128 elements is summed with eight
+// accumulators (n < 8: sequentially from -0.0); longer arrays split at n2 = n/2 - (n/2) % 8 and
+// return pw(left) + pw(right). No device recursion (it would need a runtime-sized stack): pw_tree
+// walks the same tree with an explicit stack, taking leaf sums from a callback.
+__device__ double pw_leaf(const double* a, long n, long stride) {
   if (n < 8) {
     double res = -0.0;
     for (long i = 0; i < n; i++) res += a[i * stride];
     return res;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; j++) r[j] = a[j * stride];
-    long i;
-    for (i = 8; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; j++) r[j] += a[(i + j) * stride];
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; i++) res += a[i * stride];
-    return res;
+  double r[8];
+  for (int j = 0; j < 8; j++) r[j] = a[j * stride];
+  long i;
+  for (i = 8; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; j++) r[j] += a[(i + j) * stride];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; i++) res += a[i * stride];
+  return res;
+}
+
+template <class Leaf>
+__device__ double pw_tree(long n, Leaf leaf) {
+  struct Fr { long off, n; double left; int state; };
+  Fr fr[40];   // depth log2(n / 128) + 1
+  int sp = 0;
+  fr[sp++] = Fr{0, n, 0.0, 0};
+  double ret = 0.0;
+  while (sp) {
+    Fr& f = fr[sp - 1];
+    if (f.n <= 128) { ret = leaf(f.off, f.n); sp--; continue; }
+    long m2 = f.n / 2;
+    m2 -= m2 % 8;
+    if (f.state == 0) { f.state = 1; fr[sp++] = Fr{f.off, m2, 0.0, 0}; continue; }
+    if (f.state == 1) { f.left = ret; f.state = 2; fr[sp++] = Fr{f.off + m2, f.n - m2, 0.0, 0}; continue; }
+    ret = f.left + ret;
+    sp--;
   }
-  long n2 = n / 2;
-  n2 -= n2 % 8;
-  return np_pairwise(a, n2, stride) + np_pairwise(a + n2 * stride, n - n2, stride);
+  return ret;
+}
+
+__device__ double np_pairwise(const double* a, long n, long stride) {
+  return pw_tree(n, [&](long off, long m) { return pw_leaf(a + off * stride, m, stride); });
+}
+
+// np_pairwise of a[0..n) by a whole block: thread 0 lists the tree's leaves (leaf: >= 2 *
+// (n / 64 + 2) ints), the block sums them in parallel (val), thread 0 combines them in the tree's
+// order. Same bits as np_pairwise; called by every thread, result returned on all.
+__device__ double block_pairwise(const double* a, long n, int* leaf, double* val, double* out) {
+  __shared__ int s_nleaf;
+  if (threadIdx.x == 0) {
+    int nl = 0;
+    pw_tree(n, [&](long off, long m) { leaf[2 * nl] = (int)off; leaf[2 * nl + 1] = (int)m; nl++; return 0.0; });
+    s_nleaf = nl;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s_nleaf; i += blockDim.x) val[i] = pw_leaf(a + leaf[2 * i], leaf[2 * i + 1], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int next = 0;
+    *out = pw_tree(n, [&](long, long) { return val[next++]; });
+  }
+  __syncthreads();
+  return *out;
 }
 
 __device__ __forceinline__ double sigmoid_np(double x) {  // ls/policy/network.py:132-138
@@ -84,6 +126,10 @@ struct PolicyBufs {
   double* scratch;                                  // [G] x 4 work arrays
   double* state;                                    // [16] baseline, best cost, entropy, ...
   int* flags;                                       // [4] non-finite flags
+  double* dz;                                       // [L][G4] BPTT gate gradients
+  unsigned long long* ctr;                          // [2] next round (1-based), draws consumed
+  int* pw_leaf;                                     // block_pairwise leaf table
+  double* pw_val;                                   // block_pairwise leaf sums
 };
 
 // ---------------------------------------------------------------- K4: forward
@@ -198,10 +244,12 @@ __global__ void forward_kernel(PolicyDims d, PolicyBufs b, double temperature) {
 
 // plan g, layer t consumes draw (first_draw + g*L + t) of the PCG64 stream: one
 // Generator.random() per Generator.choice(T, p) (ls/policy/network.py:258).
-__global__ void sample_kernel(PolicyDims d, const double* cdf, u128 state0, u128 inc, u128 first_draw,
-                              long n, uint8_t* plans) {
+// first_draw == ~0: the policy's device counter (draws consumed by earlier rounds)
+__global__ void sample_kernel(PolicyDims d, const double* cdf, const unsigned long long* ctr, u128 state0,
+                              u128 inc, u128 first_draw, long n, uint8_t* plans) {
   const long g = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
+  if (first_draw == (u128)~0ull) first_draw = ctr[1];
   u128 s = pcg_advance(state0, inc, first_draw + (u128)g * (u128)d.L);
   const u128 M = pcg_mult();
   for (int t = 0; t < d.L; t++) {
@@ -228,27 +276,69 @@ struct RoundIn {
   long long* best_where; // [2]: round, index
 };
 
-// state[0] baseline, state[1] best cost (+inf before round 1), state[2] entropy of the round
-__global__ void round_update_kernel(PolicyDims d, PolicyBufs b, RoundIn in) {
-  __shared__ double sh[64];
+// block-wide reductions (order-independent ops only: min / max / or)
+template <bool MAX>
+__device__ double block_minmax_d(double v, double* red) {
+  for (int o = 16; o; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = MAX ? (u > v ? u : v) : (u < v ? u : v);
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); i++) r = MAX ? (red[i] > r ? red[i] : r) : (red[i] < r ? red[i] : r);
+  __syncthreads();
+  return r;
+}
+
+__device__ long block_min_l(long v, long* red) {
+  for (int o = 16; o; o >>= 1) {
+    const long u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u < v ? u : v;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  long r = red[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); i++) r = red[i] < r ? red[i] : r;
+  __syncthreads();
+  return r;
+}
+
+// state[0] baseline, state[1] best cost (+inf before round 1), state[2] entropy of the round.
+// One block of kRoundThreads threads. Every step is either elementwise (parallel), an
+// order-independent min/max (block reductions), numpy's pairwise sum (block_pairwise: same
+// recursion, leaves in parallel) or the trace-order dlogits accumulation (one thread per (t, a),
+// sequential over g as numpy's `dlogits += ...` loop; its terms are precomputed in parallel).
+constexpr int kRoundThreads = 1024;
+__global__ void __launch_bounds__(kRoundThreads) round_update_kernel(PolicyDims d, PolicyBufs b, RoundIn in) {
+  __shared__ double sh[8];
+  __shared__ double red[32];
+  __shared__ long redl[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const long G = in.G;
+  const int LT = d.L * d.T;
   double* R = b.scratch;           // rewards after winsorising
-  double* X = b.scratch + G;       // R - baseline, then standardised weights
-  double* W = b.scratch + 2 * G;   // scratch
+  double* X = b.scratch + G;       // R - baseline, then the gradient weights
+  double* W = b.scratch + 2 * G;   // squared deviations
+  double* TERM = b.scratch + 4 * G;  // [L*T][G] dlogits terms
   const double base = b.state[0];
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  // best-ever: first plan (trace order) with cost < best so far (training.py:219-220)
-  if (tid == 0) {
-    double bc = b.state[1];
-    long bi = -1;
-    for (long g = 0; g < G; g++)
-      if (in.cost[g] < bc) { bc = in.cost[g]; bi = g; }
-    if (bi >= 0) {
-      b.state[1] = bc;
-      for (int t = 0; t < d.L; t++) in.best_plan[t] = in.plans[bi * d.L + t];
-      in.best_where[0] = in.round;
-      in.best_where[1] = bi;
+  const int round = (in.round > 0) ? in.round : (int)b.ctr[0];
+  // best-ever: the first plan (trace order) reaching the round's minimum, if it beats the best
+  // so far (training.py:219-220: strict <, sequential = first index of the minimum)
+  double mn = inf;
+  for (long g = tid; g < G; g += nt) mn = in.cost[g] < mn ? in.cost[g] : mn;
+  mn = block_minmax_d<false>(mn, red);
+  const double bc = b.state[1];
+  if (mn < bc) {
+    long first = G;
+    for (long g = tid; g < G; g += nt) if (in.cost[g] == mn && g < first) first = g;
+    first = block_min_l(first, redl);
+    for (int t = tid; t < d.L; t += nt) in.best_plan[t] = in.plans[first * d.L + t];
+    if (tid == 0) {
+      b.state[1] = mn;
+      in.best_where[0] = round;
+      in.best_where[1] = first;
     }
   }
   // rewards; any infeasible?
@@ -259,26 +349,23 @@ __global__ void round_update_kernel(PolicyDims d, PolicyBufs b, RoundIn in) {
   }
   any_bad = __syncthreads_or(any_bad);
   if (any_bad) {  // winsorise penalised rewards into [b-2u, b-u] (training.py:221-240)
-    if (tid == 0) {
-      double spread = -inf, lo = inf, hi = -inf;
-      bool have = false;
-      for (long g = 0; g < G; g++) {
-        const bool ok = (in.status[g] & 0x7f) == HPS_ST_OK;
-        if (ok) {
-          const double v = fabs(R[g] - base);
-          if (!have || v > spread) spread = v;
-          have = true;
-        } else {
-          if (R[g] < lo) lo = R[g];
-          if (R[g] > hi) hi = R[g];
-        }
+    double spread = -inf, lo = inf, hi = -inf;
+    int have = 0;
+    for (long g = tid; g < G; g += nt) {
+      if ((in.status[g] & 0x7f) == HPS_ST_OK) {
+        const double v = fabs(R[g] - base);
+        spread = v > spread ? v : spread;
+        have = 1;
+      } else {
+        lo = R[g] < lo ? R[g] : lo;
+        hi = R[g] > hi ? R[g] : hi;
       }
-      sh[0] = 10.0 * (have ? spread : 1.0);
-      sh[1] = lo;
-      sh[2] = hi;
     }
-    __syncthreads();
-    const double unit = sh[0], lo = sh[1], hi = sh[2];
+    spread = block_minmax_d<true>(spread, red);
+    lo = block_minmax_d<false>(lo, red);
+    hi = block_minmax_d<true>(hi, red);
+    have = __syncthreads_or(have);
+    const double unit = 10.0 * (have ? spread : 1.0);
     for (long g = tid; g < G; g += nt)
       if ((in.status[g] & 0x7f) != HPS_ST_OK) {
         const double z = (hi == lo) ? 0.5 : (R[g] - lo) / (hi - lo);
@@ -288,19 +375,12 @@ __global__ void round_update_kernel(PolicyDims d, PolicyBufs b, RoundIn in) {
   }
   for (long g = tid; g < G; g += nt) X[g] = R[g] - base;
   __syncthreads();
-  if (tid == 0) {  // np.std(R - b) and np.mean(R), np.mean(cost) (pairwise)
-    const double mean = np_pairwise(X, G, 1) / (double)G;
-    sh[3] = mean;
-  }
+  // np.std(R - b) (pairwise mean, pairwise sum of squares) and np.mean(R)
+  const double mean = block_pairwise(X, G, b.pw_leaf, b.pw_val, &sh[0]) / (double)G;
+  for (long g = tid; g < G; g += nt) { const double v = X[g] - mean; W[g] = v * v; }
   __syncthreads();
-  for (long g = tid; g < G; g += nt) { const double v = X[g] - sh[3]; W[g] = v * v; }
-  __syncthreads();
-  if (tid == 0) {
-    sh[4] = sqrt(np_pairwise(W, G, 1) / (double)G);
-    sh[5] = np_pairwise(R, G, 1) / (double)G;  // mean reward
-  }
-  __syncthreads();
-  const double spread = sh[4];
+  const double spread = sqrt(block_pairwise(W, G, b.pw_leaf, b.pw_val, &sh[1]) / (double)G);
+  const double mean_r = block_pairwise(R, G, b.pw_leaf, b.pw_val, &sh[2]) / (double)G;
   const double scale = 1.0 / (double)G;
   for (long g = tid; g < G; g += nt) {  // gradient weights (training.py:245-252, 136-137)
     double r2 = R[g];
@@ -308,52 +388,62 @@ __global__ void round_update_kernel(PolicyDims d, PolicyBufs b, RoundIn in) {
     X[g] = (r2 - base) * scale;
   }
   __syncthreads();
-  // dlogits accumulated in trace order (training.py:134-143); one thread per (t, a)
-  for (int e = tid; e < d.L * d.T; e += nt) {
-    const int t = e / d.T, a = e % d.T;
-    const double p = b.probs[e];
+  // dlogits terms (weight * (onehot - probs)) / temperature, all (t, a, g) in parallel
+  for (long q = tid; q < (long)LT * G; q += nt) {
+    const int e = (int)(q / G);
+    const long g = q - (long)e * G;
+    const int t = e / d.T, a = e - t * d.T;
+    const double oh = (in.plans[g * d.L + t] == a) ? 1.0 : 0.0;
+    TERM[q] = X[g] * (oh - b.probs[e]) / in.temperature;
+  }
+  __syncthreads();
+  // accumulated in trace order (training.py:134-143): dlogits += term_g, g = 0, 1, ...
+  for (int e = tid; e < LT; e += nt) {
+    const double* row = TERM + (long)e * G;
     double acc = 0.0;
-    for (long g = 0; g < G; g++) {
-      const double oh = (in.plans[g * d.L + t] == a) ? 1.0 : 0.0;
-      acc = acc + X[g] * (oh - p) / in.temperature;
-    }
+    for (long g = 0; g < G; g++) acc = acc + row[g];
     b.dlogits[e] = acc;
   }
+  const double mean_cost = block_pairwise(in.cost, G, b.pw_leaf, b.pw_val, &sh[3]) / (double)G;
   if (tid == 0) {
-    const double mean_cost = np_pairwise(in.cost, G, 1) / (double)G;
-    const double nb = (1.0 - in.gamma) * base + in.gamma * sh[5];
+    const double nb = (1.0 - in.gamma) * base + in.gamma * mean_r;
     b.state[0] = nb;
-    double* hrow = in.history + (long)(in.round - 1) * 4;
+    double* hrow = in.history + (long)(round - 1) * 4;
     hrow[0] = mean_cost;
     hrow[1] = b.state[1];
     hrow[2] = nb;
     hrow[3] = b.state[2];
+    b.ctr[0] = (unsigned long long)round + 1;   // device round counter (graph-replayed rounds)
+    b.ctr[1] += (unsigned long long)G * d.L;
   }
+}
+
+__global__ void set_ctr_kernel(unsigned long long* ctr, unsigned long long round, unsigned long long draws) {
+  ctr[0] = round;
+  ctr[1] = draws;
 }
 
 // ---------------------------------------------------------------- K5: BPTT + update
 
-__global__ void backward_kernel(PolicyDims d, PolicyBufs b) {  // network.py:203-248
+// BPTT (network.py:203-248) split in two. bptt_kernel (one block) runs the sequential recurrence
+// dh -> gates -> dz -> dh_next and stores dz for every step; grads_kernel (whole grid) then forms
+// the weight gradients as the reference accumulates them: grads.w_cell[k][j] = sum over
+// t = L-1 .. 0 of xh_t[k] * dz_t[j], product rounded, then added, in that order (np.outer then
+// +=), so every element is the reference's bits given the same dz. (A DMMA tile would fuse
+// product and sum into one rounding per k-step and lose that; the accumulation is 16 steps
+// per element, memory-light, and parallel over 36 K elements, so CUDA cores are the right unit.)
+__global__ void bptt_kernel(PolicyDims d, PolicyBufs b) {
   extern __shared__ double sm[];
-  const int H = d.H, D = d.D, G4 = d.G4, T = d.T, DH = D + H;
+  const int H = d.H, D = d.D, G4 = d.G4, T = d.T;
   double* dhn = sm;          // [H] dh_next
   double* dcn = dhn + H;     // [H] dc_next
   double* dz = dcn + H;      // [G4]
   double* dh = dz + G4;      // [H]
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int i = tid; i < H; i += nt) { dhn[i] = 0.0; dcn[i] = 0.0; }
-  for (long e = tid; e < (long)DH * G4; e += nt) b.gw_cell[e] = 0.0;
-  for (int e = tid; e < G4; e += nt) b.gb_cell[e] = 0.0;
-  for (int e = tid; e < H * T; e += nt) b.gw_out[e] = 0.0;
-  for (int e = tid; e < T; e += nt) b.gb_out[e] = 0.0;
   __syncthreads();
   for (int t = d.L - 1; t >= 0; t--) {
     const double* dl = b.dlogits + t * T;
-    for (int e = tid; e < H * T; e += nt) {  // grads.w_out += outer(h, dl)
-      const int i = e / T, a = e % T;
-      b.gw_out[e] = b.gw_out[e] + b.hh[t * H + i] * dl[a];
-    }
-    for (int a = tid; a < T; a += nt) b.gb_out[a] = b.gb_out[a] + dl[a];
     for (int i = tid; i < H; i += nt) {  // dh = W_out @ dl + dh_next
       double acc = 0.0;
       for (int a = 0; a < T; a++) acc = fma(b.w_out[i * T + a], dl[a], acc);
@@ -378,19 +468,43 @@ __global__ void backward_kernel(PolicyDims d, PolicyBufs b) {  // network.py:203
       }
     }
     __syncthreads();
-    const double* xh = b.xh + t * DH;
-    for (long e = tid; e < (long)DH * G4; e += nt) {  // grads.w_cell += outer(xh, dz)
-      const int k = (int)(e / G4), jj = (int)(e % G4);
-      b.gw_cell[e] = b.gw_cell[e] + xh[k] * dz[jj];
-    }
-    for (int jj = tid; jj < G4; jj += nt) b.gb_cell[jj] = b.gb_cell[jj] + dz[jj];
-    __syncthreads();
-    for (int i = tid; i < H; i += nt) {  // dh_next = (W_cell @ dz)[D:]
+    for (int jj = tid; jj < G4; jj += nt) b.dz[t * G4 + jj] = dz[jj];
+    // dh_next = (W_cell @ dz)[D:]: one warp per row, lanes over the G4 columns
+    for (int i = warp; i < H; i += nw) {
+      const double* wrow = b.w_cell + (long)(D + i) * G4;
       double acc = 0.0;
-      for (int jj = 0; jj < G4; jj++) acc = fma(b.w_cell[(long)(D + i) * G4 + jj], dz[jj], acc);
-      dhn[i] = acc;
+      for (int jj = lane; jj < G4; jj += 32) acc = fma(wrow[jj], dz[jj], acc);
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) dhn[i] = acc;
     }
     __syncthreads();
+  }
+}
+
+// grads.w_cell += outer(xh_t, dz_t), grads.b_cell += dz_t, grads.w_out += outer(h_t, dl_t),
+// grads.b_out += dl_t for t = L-1 .. 0, one thread per gradient element (grads start at zero)
+__global__ void grads_kernel(PolicyDims d, PolicyBufs b) {
+  const int G4 = d.G4, H = d.H, T = d.T, DH = d.D + d.H;
+  const long n1 = (long)DH * G4, n2 = n1 + G4, n3 = n2 + (long)H * T, n4 = n3 + T;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (e < n1) {
+      const int k = (int)(e / G4), j = (int)(e - (long)k * G4);
+      for (int t = d.L - 1; t >= 0; t--) acc = acc + b.xh[t * DH + k] * b.dz[t * G4 + j];
+      b.gw_cell[e] = acc;
+    } else if (e < n2) {
+      const int j = (int)(e - n1);
+      for (int t = d.L - 1; t >= 0; t--) acc = acc + b.dz[t * G4 + j];
+      b.gb_cell[j] = acc;
+    } else if (e < n3) {
+      const int q = (int)(e - n2), i = q / T, a = q - i * T;
+      for (int t = d.L - 1; t >= 0; t--) acc = acc + b.hh[t * H + i] * b.dlogits[t * T + a];
+      b.gw_out[q] = acc;
+    } else {
+      const int a = (int)(e - n3);
+      for (int t = d.L - 1; t >= 0; t--) acc = acc + b.dlogits[t * T + a];
+      b.gb_out[a] = acc;
+    }
   }
 }
 
@@ -464,12 +578,21 @@ int hps_policy_create(int32_t L, int32_t D, int32_t H, int32_t T, int32_t lstm, 
   rc |= palloc(p, &b.xh, (size_t)L * DH);
   for (double** q : {&b.gi, &b.gf, &b.go, &b.gg, &b.cc, &b.cp, &b.tc, &b.hh}) rc |= palloc(p, q, (size_t)L * H);
   rc |= palloc(p, &b.probs, (size_t)L * T);     rc |= palloc(p, &b.cdf, (size_t)L * T);
-  rc |= palloc(p, &b.dlogits, (size_t)L * T);   rc |= palloc(p, &b.scratch, (size_t)max_plans * 4);
+  rc |= palloc(p, &b.dlogits, (size_t)L * T);
+  rc |= palloc(p, &b.scratch, (size_t)max_plans * (4 + (size_t)L * T));
   rc |= palloc(p, &b.state, 16);                rc |= palloc(p, &b.flags, 4);
-  if (rc) return HPS_E_CUDA;
-  PCUDA(cudaMemcpy(b.feat, features, sizeof(double) * L * D, cudaMemcpyHostToDevice));
+  rc |= palloc(p, &b.dz, (size_t)L * G4);       rc |= palloc(p, &b.ctr, 2);
+  rc |= palloc(p, &b.pw_leaf, (size_t)2 * (max_plans / 64 + 4));
+  rc |= palloc(p, &b.pw_val, (size_t)(max_plans / 64 + 4));
+  if (rc) { hps_policy_destroy(p); return HPS_E_CUDA; }
   const double init_state[3] = {0.0, __builtin_inf(), 0.0};
-  PCUDA(cudaMemcpy(b.state, init_state, sizeof(init_state), cudaMemcpyHostToDevice));
+  const unsigned long long init_ctr[2] = {1ull, 0ull};
+  if (cudaMemcpy(b.feat, features, sizeof(double) * L * D, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(b.state, init_state, sizeof(init_state), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(b.ctr, init_ctr, sizeof(init_ctr), cudaMemcpyHostToDevice) != cudaSuccess) {
+    hps_policy_destroy(p);
+    return perr(HPS_E_CUDA, "policy upload failed");
+  }
   *out = p;
   return HPS_OK;
 }
@@ -518,8 +641,9 @@ int hps_policy_sample(HpsPolicy* p, const HpsPcg64* gen, uint64_t first_draw, in
   if (n == 0) return HPS_OK;
   const u128 s0 = ((u128)gen->state_hi << 64) | gen->state_lo, inc = ((u128)gen->inc_hi << 64) | gen->inc_lo;
   HPS_COUNT_LAUNCH();
-  sample_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(p->d, p->b.cdf, s0, inc,
-                                                                               (u128)first_draw, n, d_plans);
+  const u128 fd = (first_draw == ~0ull) ? (u128)~0ull : (u128)first_draw;
+  sample_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(p->d, p->b.cdf, p->b.ctr, s0, inc,
+                                                                               fd, n, d_plans);
   PCUDA(cudaGetLastError());
   return HPS_OK;
 }
@@ -536,14 +660,28 @@ int hps_policy_reinforce(HpsPolicy* p, const double* d_cost, const uint8_t* d_st
   cudaStream_t st = (cudaStream_t)stream;
   RoundIn in{d_cost, d_status, d_plans, G, temperature, lr, gamma, round, d_history, d_best_plan, d_best_where};
   HPS_COUNT_LAUNCH();
-  round_update_kernel<<<1, 256, 0, st>>>(p->d, p->b, in);
+  round_update_kernel<<<1, kRoundThreads, 0, st>>>(p->d, p->b, in);
   PCUDA(cudaGetLastError());
   const size_t smem = sizeof(double) * (3 * p->d.H + p->d.G4);
   HPS_COUNT_LAUNCH();
-  backward_kernel<<<1, 512, smem, st>>>(p->d, p->b);
+  bptt_kernel<<<1, 512, smem, st>>>(p->d, p->b);
+  PCUDA(cudaGetLastError());
+  const long ngrad = (long)(p->d.D + p->d.H) * p->d.G4 + p->d.G4 + (long)p->d.H * p->d.T + p->d.T;
+  HPS_COUNT_LAUNCH();
+  grads_kernel<<<(unsigned)((ngrad + 255) / 256), 256, 0, st>>>(p->d, p->b);
   PCUDA(cudaGetLastError());
   HPS_COUNT_LAUNCH();
   update_kernel<<<1, 1024, 0, st>>>(p->d, p->b, lr);
+  PCUDA(cudaGetLastError());
+  return HPS_OK;
+}
+
+// device round counter read by hps_policy_sample (first_draw = ~0) and hps_policy_reinforce
+// (round = 0), advanced by every reinforce: lets a captured round be replayed unchanged
+int hps_policy_counter(HpsPolicy* p, uint64_t round, uint64_t draws, void* stream) {
+  if (!p || round < 1) return perr(HPS_E_INVALID_ARG, "bad counter");
+  HPS_COUNT_LAUNCH();
+  set_ctr_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(p->b.ctr, round, draws);
   PCUDA(cudaGetLastError());
   return HPS_OK;
 }

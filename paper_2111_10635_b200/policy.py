@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import math
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Callable
@@ -223,6 +224,9 @@ def init_policy(graph, catalog, config: TrainerConfig):
 
 # ----------------------------------------------------------------------------- device policy
 
+_DEVICE_COUNTER = (1 << 64) - 1   # hps_policy_sample first_draw: read the device counter
+
+
 def _lib():
     return _abi.load_library()
 
@@ -305,6 +309,9 @@ class DevicePolicy:
             C.c_void_p(history.data_ptr()), C.c_void_p(best_plan.data_ptr()),
             C.c_void_p(best_where.data_ptr()), self._stream()), "hps_policy_reinforce")
 
+    def set_counter(self, round_index: int, draws: int):
+        _chk(self.lib.hps_policy_counter(self.h, round_index, draws, self._stream()), "hps_policy_counter")
+
     def state(self):
         st = (C.c_double * 3)()
         fl = (C.c_int32 * 2)()
@@ -379,12 +386,48 @@ def train(graph, catalog, params0: PolicyParams, config: TrainerConfig, job,
     recorded = torch.empty((config.rounds, G, L), dtype=torch.uint8, device=dev) if record_plans else None
     draws = 0      # 64-bit draws consumed by Generator.random() so far
     halves = 0     # 32-bit halves consumed by Generator.integers() (warm-up rounds)
+    # HPS_RL_GRAPH=1: on-policy rounds (device scorer, one rank) are captured once as a CUDA
+    # graph and replayed; the round number and the PCG64 draw offset live in the policy's device
+    # counter, so every replay is the next round. Off by default: a round is device-bound
+    # (1.16 ms replayed vs 1.19 ms eager on cfg4) and the capture costs ~17 ms up front, which
+    # time-to-best pays (tools/rl_rounds.py; profiles/r2_rl_rounds.log).
+    use_graph = (device_scoring and world == 1 and config.rounds > config.warmup_rounds
+                 and os.environ.get("HPS_RL_GRAPH", "0") == "1")
+    cuda_graph = None
+
+    def on_policy_round():   # forward, sample, score, REINFORCE: stream-ordered, no host sync
+        dp.forward(config.temperature)
+        dp.sample(pcg, _DEVICE_COUNTER, G, plans)
+        out = inst.score(plans, want_k=False)
+        cost.copy_(out["cost"])
+        status.copy_(out["status"])
+        dp.reinforce(cost, status, plans, 0, config.temperature, config.learning_rate,
+                     config.baseline_rate, history, best_plan, best_where)
+
     # round_wall_s[r-1]: seconds from the start of round 1 to the END of round r on the device
     # timeline (CUDA events on the launching stream, read after the final synchronize)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev0.record()
     round_events = []
     for r in range(1, config.rounds + 1):
+        if use_graph and r > config.warmup_rounds:
+            if cuda_graph is None:
+                dp.set_counter(r, draws)
+                inst.score(plans, want_k=False)   # first-call setup outside the capture
+                torch.cuda.current_stream().synchronize()
+                cuda_graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(cuda_graph):
+                    on_policy_round()
+            cuda_graph.replay()
+            draws += G * L
+            if recorded is not None:
+                recorded[r - 1].copy_(plans)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            round_events.append(ev)
+            if r % 16 == 0 or r == config.rounds:
+                torch.cuda.current_stream().synchronize()
+            continue
         dp.forward(config.temperature)
         if r <= config.warmup_rounds:
             if T & (T - 1):

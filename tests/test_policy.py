@@ -67,3 +67,43 @@ def test_training_rounds_match_reference(idx):
     assert res.best.cost.hex() == tr["best_cost"]
     final_norm = float(np.linalg.norm(res.params.flat()))
     assert abs(final_norm - float.fromhex(tr["final_params_norm"])) <= 1e-9 * final_norm
+
+
+@pytest.mark.gpu
+def test_graph_replayed_rounds_equal_eager_rounds(monkeypatch):
+    """The CUDA-graph round (device round counter) and the eager round run the same kernels."""
+    g, c, job = instance("cfg1")
+    cfg = pol.TrainerConfig(rounds=40, plans_per_round=64, seed=1)
+    params0, _ = pol.init_policy(g, c, cfg)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HPS_RL_GRAPH", mode)   # eager / CUDA-graph replay
+        out[mode] = pol.train(g, c, params0, cfg, job, record_plans=True)
+    a, b = out["0"], out["1"]
+    assert np.array_equal(a.sampled_plans, b.sampled_plans)
+    assert [h.baseline.hex() for h in a.history] == [h.baseline.hex() for h in b.history]
+    assert np.array_equal(a.params.flat(), b.params.flat())
+
+
+CFG4_FULL = GOLDEN / "rl_traces_cfg4_200.json.gz"
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not CFG4_FULL.exists(), reason="cfg4 200-round golden not generated")
+def test_cfg4_all_200_rounds_match_reference():
+    """BASELINE cfg4 (CTRDNN16, 4096 plans x 200 rounds): every round's sampled plans, costs and
+    baseline equal the reference trainer's (tests/golden/make_rl_goldens.py --cfg4-full)."""
+    with gzip.open(CFG4_FULL, "rt") as f:
+        tr = json.load(f)
+    g, c, job = instance(tr["instance"])
+    cfg = pol.TrainerConfig(rounds=tr["rounds"], plans_per_round=tr["plans_per_round"], seed=tr["seed"])
+    params0, _ = pol.init_policy(g, c, cfg)
+    res = pol.train(g, c, params0, cfg, job, record_plans=True)
+    for r, (h, st) in enumerate(zip(tr["history"], res.history)):
+        assert hashlib.sha1(res.sampled_plans[r].tobytes()).hexdigest() == h["plans_sha1"], r + 1
+        assert st.mean_cost.hex() == h["mean_cost"] and st.best_cost.hex() == h["best_cost"], r + 1
+        assert st.baseline.hex() == h["baseline"], r + 1
+        assert abs(st.entropy - float.fromhex(h["entropy"])) <= 1e-12 * abs(st.entropy)
+    assert list(res.best.plan.assignment) == tr["best_plan"]
+    final_norm = float(np.linalg.norm(res.params.flat()))
+    assert abs(final_norm - float.fromhex(tr["final_params_norm"])) <= 1e-9 * final_norm
