@@ -263,11 +263,13 @@ eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
 
 // _CostModel.real_cost (ls/provisioner.py:230-249), evaluated by one warp: lanes compute the
 // stages' real counts and times; the per_second sum stays CPython's sequential Neumaier sum in
-// stage order (lane 0), so the value is bit-identical to the reference's.
+// stage order (lane 0), so the value is bit-identical to the reference's. Each warp of the slow
+// block has its own term row, so the block evaluates up to 8 points at once.
 __device__ double real_cost_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double tau) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  __shared__ double terms[2][64];  // per warp-0 use only (the slow kernel calls it from warp 0)
+  __shared__ double terms_all[kSlowThreads / 32][64];
+  double* terms = terms_all[threadIdx.x >> 5];
   bool raised = false;
   double et = 0.0;
   for (int s = lane; s < S; s += 32) {
@@ -275,7 +277,7 @@ __device__ double real_cost_dev(const InstanceConsts& c, const WarpSmem<64>& w, 
     if (!floor_count(w.st[s], tau, c.bo, r, g)) { raised = true; continue; }
     const double k = pmax(1.0, r);
     et = fmax(et, stage_et(w.st[s], k));  // max over stages: order-free
-    terms[0][s] = c.price_s[w.st[s].type] * k;
+    terms[s] = c.price_s[w.st[s].type] * k;
   }
   if (__any_sync(0xffffffffu, raised)) return inf;
   et = warp_max(et);
@@ -290,7 +292,7 @@ __device__ double real_cost_dev(const InstanceConsts& c, const WarpSmem<64>& w, 
         out = inf;
       } else {
         PySum ps;
-        for (int s = 0; s < S; s++) ps.add(terms[0][s]);
+        for (int s = 0; s < S; s++) ps.add(terms[s]);
         out = c.work / thr * ps.result();
       }
     }
@@ -298,14 +300,37 @@ __device__ double real_cost_dev(const InstanceConsts& c, const WarpSmem<64>& w, 
   return __shfl_sync(0xffffffffu, out, 0);
 }
 
-__device__ bool newton_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double lo, double hi,
-                           double& xo) {  // _newton_minimize (ls/provisioner.py:317-345)
+// Block-parallel continuous search of the >4096-breakpoint path. The reference's sequence of
+// points and comparisons is kept exactly; only independent real_cost evaluations run on
+// different warps at the same time.
+struct SlowSearch {
+  double x[kSlowThreads / 32];   // points evaluated this round (one per warp)
+  double f[kSlowThreads / 32];
+};
+
+// every warp w < n evaluates x[w] into f[w]
+__device__ __forceinline__ void eval_points(const InstanceConsts& c, const WarpSmem<64>& w, int S, SlowSearch& ss,
+                                            int n) {
+  const int warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (warp < n) {
+    const double v = real_cost_dev(c, w, S, ss.x[warp]);
+    if ((threadIdx.x & 31) == 0) ss.f[warp] = v;
+  }
+  __syncthreads();
+}
+
+// _newton_minimize (ls/provisioner.py:317-345): the three finite-difference points of an
+// iteration are evaluated by three warps; the convergence check's point follows.
+__device__ bool newton_block(const InstanceConsts& c, const WarpSmem<64>& w, int S, double lo, double hi,
+                             SlowSearch& ss, double& xo) {
   const double h = pmax(c.fd_step * (hi - lo), 1e-12);
   double x = pmin(hi - h, lo + pmax(h, (hi - lo) * 0.25));
   if (x <= lo + h) return false;
   for (int it = 0; it < c.newton_max_iters; it++) {
-    const double fm = real_cost_dev(c, w, S, x - h), f0 = real_cost_dev(c, w, S, x),
-                 fp = real_cost_dev(c, w, S, x + h);
+    if (threadIdx.x == 0) { ss.x[0] = x - h; ss.x[1] = x; ss.x[2] = x + h; }
+    eval_points(c, w, S, ss, 3);
+    const double fm = ss.f[0], f0 = ss.f[1], fp = ss.f[2];
     if (!(isfinite(fm) && isfinite(f0) && isfinite(fp))) return false;
     const double d1 = (fp - fm) / (2.0 * h);
     const double d2 = (fp - 2.0 * f0 + fm) / (h * h);
@@ -314,7 +339,9 @@ __device__ bool newton_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S
     const double xn = x - step;
     if (!isfinite(xn) || xn < lo || xn > hi) return false;
     if (fabs(xn - x) < c.newton_tol * pmax(1.0, fabs(x))) {
-      if (real_cost_dev(c, w, S, xn) <= f0 + 1e-12) { xo = xn; return true; }
+      if (threadIdx.x == 0) ss.x[0] = xn;
+      eval_points(c, w, S, ss, 1);
+      if (ss.f[0] <= f0 + 1e-12) { xo = xn; return true; }
       return false;
     }
     x = xn;
@@ -322,32 +349,66 @@ __device__ bool newton_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S
   return false;
 }
 
-__device__ double golden_dev(const InstanceConsts& c, const WarpSmem<64>& w, int S, double lo, double hi) {
-  // _golden_minimize (ls/provisioner.py:348-371)
+// _golden_minimize (ls/provisioner.py:348-371). The 17-point scan is evaluated 8 points at a
+// time. Each golden iteration evaluates one new point whose position depends on the earlier
+// comparisons; the block evaluates the 7 candidate points of the next 3 iterations (the binary
+// tree of outcomes of iterations 2 and 3; iteration 1's outcome is already known) and then
+// replays the 3 iterations exactly, so 60 iterations take 20 rounds of evaluation.
+__device__ double golden_block(const InstanceConsts& c, const WarpSmem<64>& w, int S, double lo, double hi,
+                               SlowSearch& ss) {
   if (hi <= lo) return lo;
-  const int n = 17;
-  double xs[17], vals[17];
-  for (int i = 0; i < n; i++) {
-    xs[i] = lo + (hi - lo) * (double)i / (double)(n - 1);
-    vals[i] = real_cost_dev(c, w, S, xs[i]);
+  constexpr int n = 17, kW = kSlowThreads / 32;
+  double vals[n];
+  for (int i0 = 0; i0 < n; i0 += kW) {
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kW && i0 + q < n; q++) ss.x[q] = lo + (hi - lo) * (double)(i0 + q) / (double)(n - 1);
+    eval_points(c, w, S, ss, min(kW, n - i0));
+    for (int q = 0; q < kW && i0 + q < n; q++) vals[i0 + q] = ss.f[q];
   }
   int best = 0;
   for (int i = 1; i < n; i++)
     if (vals[i] < vals[best]) best = i;
-  double a = xs[best > 0 ? best - 1 : 0], b = xs[best + 1 < n ? best + 1 : n - 1];
+  auto xs = [&](int i) { return lo + (hi - lo) * (double)i / (double)(n - 1); };   // xs[i] as the scan
+  double a = xs(best > 0 ? best - 1 : 0), b = xs(best + 1 < n ? best + 1 : n - 1);
   const double inv_phi = (sqrt(5.0) - 1.0) / 2.0;
   double cc = b - inv_phi * (b - a), dd = a + inv_phi * (b - a);
-  double fc = real_cost_dev(c, w, S, cc), fd = real_cost_dev(c, w, S, dd);
-  for (int it = 0; it < 60; it++) {
-    if (fc <= fd) {
-      b = dd; dd = cc; fd = fc;
-      cc = b - inv_phi * (b - a);
-      fc = real_cost_dev(c, w, S, cc);
-    } else {
-      a = cc; cc = dd; fc = fd;
-      dd = a + inv_phi * (b - a);
-      fd = real_cost_dev(c, w, S, dd);
+  if (threadIdx.x == 0) { ss.x[0] = cc; ss.x[1] = dd; }
+  eval_points(c, w, S, ss, 2);
+  double fc = ss.f[0], fd = ss.f[1];
+  // one iteration of the reference's loop; `take_c` = (fc <= fd); returns the new point
+  struct St { double a, b, cc, dd; };
+  auto step = [&](St& t, bool take_c) {
+    if (take_c) { t.b = t.dd; t.dd = t.cc; t.cc = t.b - inv_phi * (t.b - t.a); return t.cc; }
+    t.a = t.cc; t.cc = t.dd; t.dd = t.a + inv_phi * (t.b - t.a); return t.dd;
+  };
+  for (int it = 0; it < 60;) {
+    const int depth = min(3, 60 - it);
+    // tree nodes: node 0 = iteration it (outcome known); nodes 1-2 = iteration it+1 after
+    // outcome bit b1 of its comparison; nodes 3-6 = iteration it+2 after bits (b1, b2)
+    if (threadIdx.x == 0) {
+      const bool t0 = fc <= fd;
+      for (int node = 0; node < (1 << depth) - 1; node++) {
+        const int d = (node == 0) ? 0 : (node < 3 ? 1 : 2);
+        const int bits = node - ((1 << d) - 1);   // outcome bits of iterations it+1 .. it+d
+        St t{a, b, cc, dd};
+        double xn = step(t, t0);
+        for (int q = 0; q < d; q++) xn = step(t, (bits >> (d - 1 - q)) & 1);
+        ss.x[node] = xn;
+      }
     }
+    eval_points(c, w, S, ss, (1 << depth) - 1);
+    // replay the iterations with the evaluated values
+    int bits = 0;
+    for (int q = 0; q < depth; q++) {
+      const bool take_c = fc <= fd;
+      if (q > 0) bits = (bits << 1) | (take_c ? 1 : 0);
+      const int node = (q == 0) ? 0 : ((1 << q) - 1) + bits;
+      St t{a, b, cc, dd};
+      step(t, take_c);
+      a = t.a; b = t.b; cc = t.cc; dd = t.dd;
+      if (take_c) { fd = fc; fc = ss.f[node]; } else { fc = fd; fd = ss.f[node]; }
+    }
+    it += depth;
   }
   return (a + b) / 2.0;
 }
@@ -413,6 +474,9 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
   __shared__ int s_ncand, s_S, s_done;
   __shared__ PlanOut s_out;
   __shared__ u128 s_rank;
+  __shared__ int s_bnd[kMaxL + 2];
+  __shared__ int s_nseg, s_levels;
+  __shared__ SlowSearch s_search;
   extern __shared__ double s_sort[];  // kSlowSmemSort doubles: the sort runs here when it fits
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* raw = scratch + (size_t)blockIdx.x * per_block;  // [per_block/2] sort buffer
@@ -449,10 +513,30 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       const int nraw = s_ncand;
       int npow = 1;
       while (npow < nraw) npow <<= 1;
-      double* srt = (npow <= kSlowSmemSort) ? s_sort : raw;  // sort buffer: shared memory if it fits
-      // raw candidates (class leaders' breakpoints + tau_lo/tau_hi), out-of-range -> +inf
-      for (int i = tid; i < npow; i += kSlowThreads) {
-        double v = __longlong_as_double(0x7ff0000000000000LL);
+      const double inf = __longlong_as_double(0x7ff0000000000000LL);
+      // raw candidates: tau_lo, tau_hi, then each class leader's breakpoints et(m) for m from
+      // kmax down to kmin (ascending: et is non-increasing in m); values below tau_lo become
+      // -inf and above tau_hi +inf, which keeps every segment sorted
+      double* srt;
+      if (npow <= kSlowSmemSort) {
+        srt = s_sort;
+      } else {   // merge path: the segments are already sorted, so log2(#segments) merge passes
+        if (tid == 0) {   // segment boundaries: {tau_lo, tau_hi}, then every non-empty leader
+          int ns = 0;
+          s_bnd[ns++] = 0;
+          s_bnd[ns] = 2;
+          for (int r2 = 0; r2 < S; r2++)
+            if (w.pre[r2 + 1] > w.pre[r2]) s_bnd[++ns] = 2 + w.pre[r2 + 1];
+          s_nseg = ns;
+          int lv = 0;
+          while ((1 << lv) < ns) lv++;
+          s_levels = lv;
+        }
+        __syncthreads();
+        srt = (s_levels & 1) ? cand : raw;   // the last merge pass writes into raw
+      }
+      for (int i = tid; i < (srt == s_sort ? npow : nraw); i += kSlowThreads) {
+        double v = inf;
         if (i == 0) v = tau_lo;
         else if (i == 1) v = tau_hi;
         else if (i < nraw) {
@@ -460,31 +544,86 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
           int lo = 0, hi = S;  // find stage: pre[lo] <= j < pre[lo+1]
           while (hi - lo > 1) { int mid = (lo + hi) / 2; if (w.pre[mid] <= j) lo = mid; else hi = mid; }
           while (w.pre[lo + 1] <= j) lo++;
-          v = et_lookup(c, tb, w.st[lo], w.ent[lo], w.kmin[lo] + (double)(j - w.pre[lo]));
-          if (!(v >= tau_lo && v <= tau_hi)) v = __longlong_as_double(0x7ff0000000000000LL);
+          v = et_lookup(c, tb, w.st[lo], w.ent[lo], w.kmax[lo] - (double)(j - w.pre[lo]));
+          if (v < tau_lo) v = -inf;
+          else if (!(v <= tau_hi)) v = inf;
         }
         srt[i] = v;
       }
       __syncthreads();
-      for (int k = 2; k <= npow; k <<= 1)  // bitonic sort ascending (one thread per pair)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int t = tid; t < (npow >> 1); t += kSlowThreads) {
-            const int i = 2 * t - (t & (j - 1));   // lower index of pair t at distance j
-            const int l = i + j;
-            const double a = srt[i], b = srt[l];
-            const bool up = (i & k) == 0;
-            if (up ? (a > b) : (a < b)) { srt[i] = b; srt[l] = a; }
+      bool bitonic = srt == s_sort;
+      if (!bitonic) {   // every segment sorted? (et monotone in m needs alpha, beta, profiles >= 0)
+        bool bad = false;
+        int sg = 0;
+        for (int i = tid; i < nraw; i += kSlowThreads) {
+          while (s_bnd[sg + 1] <= i) sg++;
+          if (i > s_bnd[sg] && srt[i - 1] > srt[i]) bad = true;
+        }
+        if (__syncthreads_or(bad)) {   // rare: general sort in raw
+          for (int i = tid; i < npow; i += kSlowThreads) raw[i] = (i < nraw) ? srt[i] : inf;
+          __syncthreads();
+          srt = raw;
+          bitonic = true;
+        }
+      }
+      if (bitonic) {
+        for (int k = 2; k <= npow; k <<= 1)  // bitonic sort ascending (one thread per pair)
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = tid; t < (npow >> 1); t += kSlowThreads) {
+              const int i = 2 * t - (t & (j - 1));   // lower index of pair t at distance j
+              const int l = i + j;
+              const double a = srt[i], b = srt[l];
+              const bool up = (i & k) == 0;
+              if (up ? (a > b) : (a < b)) { srt[i] = b; srt[l] = a; }
+            }
+            __syncthreads();
+          }
+      } else {
+        // pairwise merges of adjacent segments (stable merge path per thread's output slice)
+        double* src = srt;
+        double* dst = (srt == raw) ? cand : raw;
+        while (s_nseg > 1) {
+          const int ns = s_nseg, n = s_bnd[ns];
+          const int per = (n + kSlowThreads - 1) / kSlowThreads;
+          int o = min(n, tid * per);
+          const int o1 = min(n, o + per);
+          int p = 0;
+          while (o < o1) {
+            while (s_bnd[min(2 * p + 2, ns)] <= o) p++;
+            const int b0 = s_bnd[2 * p], bm = s_bnd[min(2 * p + 1, ns)], b1 = s_bnd[min(2 * p + 2, ns)];
+            const double* A = src + b0;
+            const double* B = src + bm;
+            const int nA = bm - b0, nB = b1 - bm;
+            const int k = o - b0, end = min(o1, b1) - b0;
+            int lo = max(0, k - nB), hi = min(k, nA);
+            while (lo < hi) {   // merge path: A elements among the first k outputs (A first on ties)
+              const int m = (lo + hi) >> 1;
+              if (A[m] <= B[k - 1 - m]) lo = m + 1; else hi = m;
+            }
+            int ia = lo, ib = k - lo;
+            for (int q = k; q < end; q++)
+              dst[b0 + q] = (ia < nA && (ib >= nB || A[ia] <= B[ib])) ? A[ia++] : B[ib++];
+            o = b0 + end;
           }
           __syncthreads();
+          if (tid == 0) {
+            const int nn = (ns + 1) / 2;
+            for (int q = 1; q <= nn; q++) s_bnd[q] = s_bnd[min(2 * q, ns)];
+            s_nseg = nn;
+          }
+          __syncthreads();
+          double* t2 = src; src = dst; dst = t2;
         }
+        srt = src;   // == raw (level parity chosen above)
+      }
       // distinct finite values -> cand, in sorted order: rounds of kSlowThreads consecutive
       // entries (bank-conflict free), ballot + warp counts; stops at the first +inf (sorted)
       unsigned nc = 0;
-      for (int r0 = 0; r0 < npow; r0 += kSlowThreads) {
-        if (!(srt[r0] < __longlong_as_double(0x7ff0000000000000LL))) break;  // block-uniform
+      const int nsorted = bitonic ? npow : nraw;   // merged data is unpadded
+      for (int r0 = 0; r0 < nsorted; r0 += kSlowThreads) {
+        if (!(srt[r0] < inf)) break;  // block-uniform (sorted: +inf only at the end)
         const int i = r0 + tid;
-        const bool f = i < npow && srt[i] < __longlong_as_double(0x7ff0000000000000LL) &&
-                       (i == 0 || srt[i] != srt[i - 1]);
+        const bool f = i < nsorted && srt[i] < inf && srt[i] > -inf && (i == 0 || srt[i] != srt[i - 1]);
         const unsigned m = __ballot_sync(0xffffffffu, f);
         if (lane == 0) scan_tmp[warp] = __popc(m);
         __syncthreads();
@@ -502,10 +641,10 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       bool ovf = false;
       if (nc > (unsigned)kBpLimit) {  // ls/provisioner.py:456-470
         ovf = true;
-        if (warp == 0) {  // sequential search, each real_cost evaluated warp-parallel
+        {  // the reference's search, real_cost evaluations spread over the block's warps
           double ts;
-          if (!newton_dev(c, w, S, tau_lo, tau_hi, ts)) ts = golden_dev(c, w, S, tau_lo, tau_hi);
-          if (lane == 0) s_tau_star = ts;
+          if (!newton_block(c, w, S, tau_lo, tau_hi, s_search, ts)) ts = golden_block(c, w, S, tau_lo, tau_hi, s_search);
+          if (tid == 0) s_tau_star = ts;
         }
         __syncthreads();
         const double ts = s_tau_star;
