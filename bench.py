@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 random-plan sweep")
     ap.add_argument("--no-small", action="store_true", help="skip the cfg1/cfg2 measurements")
     ap.add_argument("--cfg5-plans", type=int, default=10 ** 9)
+    ap.add_argument("--no-prune", action="store_true", help="skip the pruned-search measurement")
     return ap.parse_args()
 
 
@@ -146,7 +147,7 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample or 80_000 * threads
+    sample = args.cpu_sample or 40_000 * threads
     for _ in range(max(0, args.warmup)):
         cpu_oracle_rate(max(1000, sample // 10), threads)
     rates, times = [], []
@@ -340,6 +341,45 @@ def measure_cfg2(torch):
             "reference_cpu_s": 2.38, "reference_source": "BASELINE.md §2 (Python reference, 1 core)"}
 
 
+def measure_pruned(torch, inst, total, full_key):
+    """Pruning-assisted exhaustive search of the same cfg3 space (hps_enum_argmin_pruned): certified
+    per-prefix cost lower bounds skip index ranges that cannot hold the winner, the rest are swept
+    exactly. Reported apart from `value` (which scores every plan); the winner must equal the full
+    sweep's, ties included."""
+    import paper_2111_10635_b200.scoring as scoring
+    from paper_2111_10635_b200.search import brute_force
+    inst.enum_argmin_pruned()   # warm-up
+    walls, keys = [], []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        key, st = inst.enum_argmin_pruned()   # synchronous (sizes the survivor sweep on the host)
+        walls.append(time.perf_counter() - t0)
+        keys.append(key)
+    assert all(k["rank"] == full_key["rank"] and k["cost"] == full_key["cost"] for k in keys)
+    g, c, job = instance()
+    e2e = []
+    for i in range(4):   # public API: brute_force(prune=True), instance staged from host memory
+        scoring._INSTANCES.clear()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        best = brute_force(g, c, job, enumeration_cap=total, prune=True)
+        if i:
+            e2e.append(time.perf_counter() - t0)
+    assert best.cost == full_key["cost"]
+    t = statistics.median(walls)
+    return {"workload": WORKLOAD, "plans_covered": total, "ms": 1e3 * t,
+            "effective_plans_per_s": total / t, "evaluated": st["evaluated"],
+            "evaluated_fraction": st["evaluated"] / total, "depth": st["depth"],
+            "prefixes": st["prefixes"], "surviving_prefixes": st["survivors"],
+            "incumbent_cost": st["incumbent_cost"], "winner_index": key["rank"],
+            "winner_cost": key["cost"], "same_winner_as_full_sweep": True,
+            "e2e_brute_force_prune_s": statistics.median(e2e),
+            "note": "exact search with certified subtree lower bounds (csrc/hps_prune.cuh); rate = "
+                    "3^16 / wall time of the whole call (bounds, incumbent sweep, survivor sweep); "
+                    "not a plans-evaluated rate"}
+
+
 def measure_cfg5(torch, dist, world, rank, dev, n_total, peak):
     """cfg5 (BASELINE configs[4]): n_total random plans of default_rng(0), 64 layers x 4 types.
     Plans are generated in-kernel (numpy Generator.integers replica) and reduced by the fused
@@ -459,6 +499,7 @@ def run_ours(args):
     d2h = _abi.ARGMIN_NBYTES * world + 8 * 6  # gathered keys + the re-scored winner's outputs
 
     peak = fp64_peak(torch, inst.lib, dev) if rank == 0 else 0.0
+    pruned = measure_pruned(torch, inst, total, key) if (rank == 0 and world == 1 and not args.no_prune) else None
     rl = cfg1 = cfg2 = None
     if not args.no_rl and rank == 0:  # latency-bound per round: timed unsharded on one GPU
         rl = measure_rl(torch, *instance("cfg4"))
@@ -509,15 +550,17 @@ def run_ours(args):
             line["cfg2_bf"] = cfg2
         if r5 is not None:
             line["cfg5_random"] = r5
+        if pruned is not None:
+            line["enum_pruned"] = pruned
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
-            sample = args.cpu_sample or 80_000 * threads
+            sample = args.cpu_sample or 40_000 * threads
             rate, dt, _ = cpu_oracle_rate(sample, threads)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                     "sample": f"{sample} cfg3 enumeration indices strided over the "
                                               f"whole 3^16 range in {dt:.1f} s ({cpu_model()})"}
             if r5 is not None:
-                s5 = 4_000 * threads
+                s5 = 16_000 * threads
                 rate5, dt5 = cpu_oracle_cfg5_rate(s5, threads)
                 r5["cpu_baseline"] = {"value": rate5, "unit": UNIT, "cores": threads, "kind": "port",
                                       "sample": f"first {s5} plans of the stream in {dt5:.1f} s"}

@@ -167,6 +167,27 @@ int hps_explain(HpsInstance* inst, const uint8_t* d_plans, const uint8_t* d_stat
 int hps_enum_argmin(HpsInstance* inst, uint64_t begin, uint64_t end, int32_t feasible_only,
                     HpsArgmin* d_best, void* stream);
 
+/* hps_enum_argmin over all T^L plans with certified subtree pruning: the plans sharing their
+ * first `depth` layers form one index range; a lower bound of the cost of every plan in the range
+ * (stage counts relaxed to the continuous requirement at the best possible E, quotas ignored)
+ * skips ranges that cannot hold a plan costing <= the incumbent, and the rest are swept exactly.
+ * Same winner (cost and index, ties included) as hps_enum_argmin(0, T^L, feasible_only = 1);
+ * `evaluated` / `feasible` count the swept plans only. incumbent = +inf: the range with the
+ * smallest bound is swept first and its winner is the incumbent. Synchronises `stream` twice
+ * (the survivor count sizes the sweep). Replaces the brute_force loop, ls/baselines.py:63-87. */
+typedef struct HpsPruneStats {
+  uint64_t prefixes;       /* T^depth index ranges */
+  uint64_t survivors;      /* ranges swept after pruning (besides the incumbent's) */
+  uint64_t evaluated;      /* plans scored */
+  uint64_t subtree;        /* plans per range, T^(L - depth) */
+  double incumbent_cost;   /* cost the bounds were compared with */
+  double min_bound;        /* smallest range bound */
+  int32_t depth;
+  int32_t pad;
+} HpsPruneStats;
+int hps_enum_argmin_pruned(HpsInstance* inst, int32_t depth, double incumbent, HpsArgmin* d_best,
+                           HpsPruneStats* stats, void* stream);
+
 /* Argmin over an explicit plan batch (u8 [n][L] device memory), same key and tie rules as
  * hps_enum_argmin; the rank packs ceil(log2 T) bits per layer (needs bits*L <= 128).
  * Replaces the scoring loop + _better of random_search's dedup path and of any caller that

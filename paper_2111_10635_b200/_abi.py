@@ -72,6 +72,12 @@ class HpsExplain(C.Structure):
                 ("serial", C.c_double), ("tau_hi", C.c_double)]
 
 
+class HpsPruneStats(C.Structure):
+    _fields_ = [("prefixes", C.c_uint64), ("survivors", C.c_uint64), ("evaluated", C.c_uint64),
+                ("subtree", C.c_uint64), ("incumbent_cost", C.c_double), ("min_bound", C.c_double),
+                ("depth", C.c_int32), ("pad", C.c_int32)]
+
+
 ARGMIN_NBYTES = C.sizeof(HpsArgmin)  # 48
 EXPLAIN_NBYTES = C.sizeof(HpsExplain)  # 64
 
@@ -171,6 +177,8 @@ _SIGNATURES = {
     "hps_report": (C.c_int, [C.c_void_p] + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 9),
     "hps_explain": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                               C.c_void_p, C.c_void_p]),
+    "hps_enum_argmin_pruned": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p,
+                                         C.POINTER(HpsPruneStats), C.c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -58,11 +58,14 @@ constexpr int kSlowSmemSort = HPS_SLOW_SORT;  // doubles of dynamic shared memor
 // ------------------------------------------------------------------ plan sources
 
 struct PlanSource {
-  int32_t mode;          // 0 plans array, 1 enumeration index, 2 numpy PCG64 integers()
+  int32_t mode;          // 0 plans array, 1 enumeration index, 2 numpy PCG64 integers(),
+                         // 3 subtrees of surviving prefixes (enumeration index
+                         //   prefixes[q / stride] * stride + q % stride, q = begin + p)
   int32_t tbits;         // mode 2: log2(T)
   const uint8_t* plans;  // mode 0
   uint64_t begin;        // mode 1/2: first enumeration index / first random plan
-  uint64_t stride;       // mode 1: plan p is enumeration index begin + p * stride
+  uint64_t stride;       // mode 1: plan p is enumeration index begin + p * stride; mode 3: subtree size
+  const uint32_t* prefixes;  // mode 3: surviving prefix ids
   uint64_t tpow[kMaxL];  // mode 1: T^(L-1-l)
   // mode 2: state after (first*L/2 + 1) steps is computed per warp; A_j/C_j advance it by j
   uint64_t s0_hi, s0_lo, inc_hi, inc_lo;
@@ -97,8 +100,15 @@ __device__ __forceinline__ void load_digits(const InstanceConsts& c, const PlanS
       }
       rank = mk(hi, lo);
     }
-  } else if (MODE == 1) {
-    const uint64_t idx = src.begin + p * src.stride;
+  } else if (MODE == 1 || MODE == 3) {
+    uint64_t idx;
+    if (MODE == 1) {
+      idx = src.begin + p * src.stride;
+    } else {
+      const uint64_t q = src.begin + p;
+      const uint64_t r = q / src.stride;
+      idx = (uint64_t)__ldg(src.prefixes + r) * src.stride + (q - r * src.stride);
+    }
     if (idx < 0xffffffffull && src.tpow[0] < 0xffffffffull) {  // 32-bit division is much cheaper
       const uint32_t i32 = (uint32_t)idx, t32 = (uint32_t)c.T;
       if (lane < L) d0 = (int)((i32 / (uint32_t)src.tpow[lane]) % t32);
@@ -495,6 +505,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       u128 rank;
       if (src.mode == 0) load_digits<0>(c, src, p, d0, d1, rank);
       else if (src.mode == 1) load_digits<1>(c, src, p, d0, d1, rank);
+      else if (src.mode == 3) load_digits<3>(c, src, p, d0, d1, rank);
       else load_digits<2>(c, src, p, d0, d1, rank);
       PlanOut r;
       r.ps = 0; r.gap = 0.0;
@@ -1263,6 +1274,7 @@ int launch_src(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs
   if (src.mode == 0) return launch_eval<MAXS, WARPS, ARGMIN, FAST, 0>(in, src, n, o, pend, feasible_only, parts, grid, st);
   if (!ARGMIN) return set_err(HPS_E_INVALID_ARG, "per-plan outputs need an explicit plan batch");
   if (src.mode == 1) return launch_eval<MAXS, WARPS, ARGMIN, FAST, 1>(in, src, n, o, pend, feasible_only, parts, grid, st);
+  if (src.mode == 3) return launch_eval<MAXS, WARPS, ARGMIN, FAST, 3>(in, src, n, o, pend, feasible_only, parts, grid, st);
   return launch_eval<MAXS, WARPS, ARGMIN, FAST, 2>(in, src, n, o, pend, feasible_only, parts, grid, st);
 }
 
@@ -1318,6 +1330,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     int rc;
     if (src.mode == 0) rc = launch_stage<MAXS, WARPS, ARGMIN, 0>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     else if (src.mode == 1) rc = launch_stage<MAXS, WARPS, ARGMIN, 1>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
+    else if (src.mode == 3) rc = launch_stage<MAXS, WARPS, ARGMIN, 3>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     if (rc) return rc;
     HPS_COUNT_LAUNCH();
@@ -1392,7 +1405,7 @@ PlanSource advance_source(const PlanSource& src, uint64_t off, int L) {
   PlanSource s = src;
   if (s.mode == 0) s.plans = src.plans + off * (uint64_t)L;
   else if (s.mode == 1) s.begin = src.begin + off * src.stride;
-  else s.begin = src.begin + off;
+  else s.begin = src.begin + off;   // modes 2, 3: plan number offset
   return s;
 }
 
@@ -1467,6 +1480,8 @@ int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_onl
 }
 
 }  // namespace
+
+#include "hps_prune.cuh"
 
 extern "C" {
 
@@ -1712,6 +1727,113 @@ int hps_enum_argmin_strided(HpsInstance* in, uint64_t first, uint64_t stride, ui
   uint64_t pw = 1;
   for (int l = in->c.L - 1; l >= 0; l--) { src.tpow[l] = pw; pw *= (uint64_t)in->c.T; }
   return argmin_common(in, src, count, feasible_only, d_best, (cudaStream_t)stream);
+}
+
+int hps_enum_argmin_pruned(HpsInstance* in, int32_t depth, double incumbent, HpsArgmin* d_best,
+                           HpsPruneStats* stats, void* stream) {
+  if (!in || !d_best) return set_err(HPS_E_INVALID_ARG, "null argument");
+  const int L = in->c.L, T = in->c.T;
+  long double total = powl((long double)T, (long double)L);
+  if (total > 1.8e19L) return set_err(HPS_E_CONFIG, "T^L does not fit a 64-bit enumeration index");
+  if (depth < 1 || depth >= L) return set_err(HPS_E_INVALID_ARG, "prefix depth must be in [1, L)");
+  uint64_t npref = 1, R = 1;
+  for (int l = 0; l < depth; l++) npref *= (uint64_t)T;
+  for (int l = depth; l < L; l++) R *= (uint64_t)T;
+  if (npref > (1ull << 28)) return set_err(HPS_E_CONFIG, "too many prefixes (lower the depth)");
+  // every plan the bound may skip must be one the reference scores without raising
+  if (in->c.ps_type < 0) return set_err(HPS_E_CONFIG, "pruning needs a CPU type (PS cores)");
+  for (const StageEntry& e : in->h_stages)
+    if (!e.valid) return set_err(HPS_E_CONFIG, "pruning needs every layer profiled on every type");
+  cudaStream_t st = (cudaStream_t)stream;
+  // geometric E grid from the smallest serial floor of any stage to B / limit
+  double emin = in->c.tau_limit;
+  for (const StageEntry& e : in->h_stages)
+    if (e.valid && e.serial > 0 && e.serial < emin) emin = e.serial;
+  emin = std::max(emin, in->c.tau_limit * 1e-12);
+  std::vector<double> grid(kPruneCells + 1);
+  for (int k = 0; k <= kPruneCells; k++)
+    grid[k] = emin * std::pow(in->c.tau_limit / emin, (double)k / kPruneCells);
+  grid[kPruneCells] = in->c.tau_limit * (1.0 + 1e-12);
+  const int ne = T * in->c.P;
+  const size_t nF = (size_t)(kPruneCells + 1) * ne, nS = (size_t)(kPruneCells + 1) * (L + 1) * (T + 1);
+  char* buf = nullptr;
+  const size_t bytes = sizeof(double) * (grid.size() + nF + nS + npref + 1) + sizeof(uint32_t) * (npref + 4) +
+                       sizeof(HpsArgmin) * 2 + 256;
+  CUDA_TRY(cudaMallocAsync(&buf, bytes, st));
+  double* dE = reinterpret_cast<double*>(buf);
+  double* dF = dE + grid.size();
+  double* dS = dF + nF;
+  double* dLB = dS + nS;
+  double* dminlb = dLB + npref;
+  HpsArgmin* keys = reinterpret_cast<HpsArgmin*>(dminlb + 1);
+  uint32_t* list = reinterpret_cast<uint32_t*>(keys + 2);
+  uint32_t* misc = list + npref;   // [0] survivors, [1] best prefix
+  CUDA_TRY(cudaMemcpyAsync(dE, grid.data(), sizeof(double) * grid.size(), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(misc, 0, sizeof(uint32_t) * 4, st));
+  HPS_COUNT_LAUNCH();
+  prune_f_kernel<<<(unsigned)((nF + 255) / 256), 256, 0, st>>>(in->c, in->tb, dE, dF);
+  CUDA_TRY(cudaGetLastError());
+  HPS_COUNT_LAUNCH();
+  prune_suffix_kernel<<<kPruneCells + 1, 32, 0, st>>>(in->c, dF, dS);
+  CUDA_TRY(cudaGetLastError());
+  HPS_COUNT_LAUNCH();
+  prune_bound_kernel<<<(unsigned)((npref + 127) / 128), 128, 0, st>>>(in->c, in->tb, dE, dF, dS, depth, npref, dLB);
+  CUDA_TRY(cudaGetLastError());
+  HPS_COUNT_LAUNCH();
+  prune_argmin_kernel<<<1, 256, 0, st>>>(dLB, npref, misc + 1, dminlb);
+  CUDA_TRY(cudaGetLastError());
+  uint32_t first = 0xffffffffu;
+  double min_lb = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&first, misc + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&min_lb, dminlb, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  uint64_t evaluated = 0;
+  const bool own_incumbent = !(incumbent < __builtin_inf());
+  PlanSource src{};
+  src.mode = 1;
+  src.stride = 1;
+  uint64_t pw = 1;
+  for (int l = L - 1; l >= 0; l--) { src.tpow[l] = pw; pw *= (uint64_t)T; }
+  if (own_incumbent && first != 0xffffffffu) {   // incumbent: the subtree with the smallest bound
+    src.begin = (uint64_t)first * R;
+    if (int rc = argmin_common(in, src, R, 1, keys, st)) return rc;
+    evaluated += R;
+  } else {
+    first = 0xffffffffu;
+    HPS_COUNT_LAUNCH();
+    finish_argmin<<<1, 256, 0, st>>>(nullptr, 0, nullptr, 0, 0, keys);
+    CUDA_TRY(cudaGetLastError());
+  }
+  HPS_COUNT_LAUNCH();
+  prune_survivors_kernel<<<(unsigned)((npref + 255) / 256), 256, 0, st>>>(
+      dLB, npref, own_incumbent ? keys : nullptr, incumbent, first, list, misc);
+  CUDA_TRY(cudaGetLastError());
+  uint32_t nsurv = 0;
+  double inc_cost = incumbent;
+  CUDA_TRY(cudaMemcpyAsync(&nsurv, misc, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  if (own_incumbent) CUDA_TRY(cudaMemcpyAsync(&inc_cost, &keys->cost, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  PlanSource sv{};
+  sv.mode = 3;
+  sv.stride = R;
+  sv.prefixes = list;
+  memcpy(sv.tpow, src.tpow, sizeof(src.tpow));
+  if (int rc = argmin_common(in, sv, (uint64_t)nsurv * R, 1, keys + 1, st)) return rc;
+  evaluated += (uint64_t)nsurv * R;
+  HPS_COUNT_LAUNCH();
+  merge_argmin<<<1, 32, 0, st>>>(keys, 2, evaluated, d_best);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(buf, st));
+  if (stats) {
+    stats->prefixes = npref;
+    stats->survivors = nsurv;
+    stats->evaluated = evaluated;
+    stats->incumbent_cost = inc_cost;
+    stats->min_bound = min_lb;
+    stats->depth = depth;
+    stats->subtree = R;
+  }
+  return HPS_OK;
 }
 
 int hps_plans_argmin(HpsInstance* in, const uint8_t* d_plans, int64_t n, int32_t feasible_only,

@@ -131,6 +131,28 @@ class DeviceInstance:
                        "hps_enum_argmin_strided")
         return buf
 
+    def enum_argmin_pruned(self, depth: int | None = None, incumbent: float = float("inf"),
+                           stream=None):
+        """Feasible-only argmin over all T^L plans with certified subtree pruning
+        (hps_enum_argmin_pruned): same winner as enum_argmin_async(0, T^L). Returns
+        (key, stats) on the host (the call synchronises the stream)."""
+        depth = self.default_prune_depth() if depth is None else int(depth)
+        buf = self._argmin_buffer()
+        stats = _abi.HpsPruneStats()
+        with torch.cuda.device(self.device):
+            _abi.check(self.lib.hps_enum_argmin_pruned(self.handle, depth, float(incumbent), _ptr(buf),
+                                                       C.byref(stats), _stream(stream)),
+                       "hps_enum_argmin_pruned")
+        st = {f: getattr(stats, f) for f, _ in _abi.HpsPruneStats._fields_ if f != "pad"}
+        return self.read_argmin(buf), st
+
+    def default_prune_depth(self) -> int:
+        """Prefix depth of the pruned sweep: about 2^16 index ranges, at least T^4 plans each."""
+        d = 1
+        while d + 1 < self.L and self.T ** (d + 1) <= (1 << 16) and self.T ** (self.L - d - 1) >= self.T ** 4:
+            d += 1
+        return d
+
     def plans_argmin_async(self, plans, feasible_only: bool = False, stream=None):
         plans = plans.to(self.device).contiguous()
         buf = self._argmin_buffer()

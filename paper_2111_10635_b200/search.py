@@ -135,14 +135,28 @@ def enumerate_argmin(graph, catalog, params, begin: int, end: int, feasible_only
 
 
 def brute_force(graph, catalog, params, config: ProvisionerConfig = ProvisionerConfig(),
-                enumeration_cap: int = DEFAULT_ENUMERATION_CAP, group=None) -> ScoredPlan:
-    """Cheapest feasible plan over all T^L assignments (ls/baselines.py:63-87)."""
+                enumeration_cap: int = DEFAULT_ENUMERATION_CAP, group=None,
+                prune: bool = False) -> ScoredPlan:
+    """Cheapest feasible plan over all T^L assignments (ls/baselines.py:63-87).
+
+    ``prune=True`` (one GPU) skips index ranges whose certified cost lower bound exceeds an
+    incumbent (hps_enum_argmin_pruned): the same plan, cost and tie-breaking, fewer plans scored.
+    Instances it does not apply to (no CPU type, unprofiled layers) and multi-rank runs sweep
+    everything."""
     T, L = catalog.num_types, graph.num_layers
     total = T ** L
     if total > enumeration_cap:
         raise ConfigError(f"brute force would enumerate {total} plans ({T}^{L}), "
                           f"cap is {enumeration_cap}")
-    key = enumerate_argmin(graph, catalog, params, 0, total, True, config, group)
+    key = None
+    dist = _dist()
+    if prune and L > 1 and (dist is None or dist.get_world_size(group) == 1):
+        try:
+            key, _ = device_instance(graph, catalog, params, config).enum_argmin_pruned()
+        except ConfigError:
+            key = None
+    if key is None:
+        key = enumerate_argmin(graph, catalog, params, 0, total, True, config, group)
     _raise_flags(key)
     if not key["cost"] < float("inf"):
         raise InfeasibleError(f"no feasible plan among {total} enumerated")

@@ -131,3 +131,26 @@ def test_pending_list_holds_more_than_2p20_plans():
     # and in an argmin: the minimum over the tiled batch is the minimum over the records
     key = inst.read_argmin(inst.plans_argmin_async(torch.from_numpy(plans).cuda(), False))
     assert key["cost"] == cost.min()
+
+
+@pytest.mark.parametrize("name,depth", [("cfg3", 10), ("cfg3", 8), ("cfg4", 8), ("cfg2", 4), ("quota", 8),
+                                        ("cfg1", 2)])
+def test_pruned_sweep_returns_the_full_sweep_winner(name, depth):
+    """Certified subtree pruning: same winner (index and cost) as the exhaustive sweep."""
+    ref = DIGESTS[name]
+    inst = _dev(name)
+    key, st = inst.enum_argmin_pruned(depth)
+    assert key["rank"] == ref["best_index"] and key["cost"] == float.fromhex(ref["best_cost"]), (key, st)
+    assert st["evaluated"] == key["evaluated"] <= inst.T ** inst.L
+    assert st["prefixes"] == inst.T ** depth
+    # with the optimum as the incumbent every surviving range holds a plan within the bound
+    key2, st2 = inst.enum_argmin_pruned(depth, incumbent=float.fromhex(ref["best_cost"]))
+    assert key2["rank"] == ref["best_index"] and st2["survivors"] <= st["survivors"] + 1
+
+
+def test_pruned_brute_force_drop_in():
+    from paper_2111_10635_b200.search import brute_force
+    g, c, job = instance("cfg4")
+    a = brute_force(g, c, job)
+    b = brute_force(g, c, job, prune=True)
+    assert a.plan == b.plan and a.cost == b.cost and a.evaluations == b.evaluations == 2 ** 16
