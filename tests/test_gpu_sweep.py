@@ -154,3 +154,36 @@ def test_pruned_brute_force_drop_in():
     a = brute_force(g, c, job)
     b = brute_force(g, c, job, prune=True)
     assert a.plan == b.plan and a.cost == b.cost and a.evaluations == b.evaluations == 2 ** 16
+
+
+def test_cfg5_stream_fast_literal_and_oracle():
+    """BASELINE cfg5 (64 layers x 4 types): the first 2^20 plans of default_rng(0) (the 1e9 sweep's
+    stream) scored by the fast and the literal paths are identical; a strided 1/64 sample equals the
+    oracle; the fused random_argmin equals the argmin of the scored outputs."""
+    import oracle
+    from goldens import staged
+    from paper_2111_10635_b200.instance import pcg_from_generator
+    n = 1 << 20
+    fast, lit = _dev("cfg5"), _dev("cfg5", HPS_FORCE_LITERAL=1)
+    pcg = pcg_from_generator(np.random.default_rng(0))
+    plans = fast.random_plans(pcg, 0, n)
+    a, b = fast.score(plans), lit.score(plans)
+    idx = torch.arange(n, dtype=torch.int64, device="cuda")
+    ha = plan_hashes(idx, a["cost"], a["status"], a["gap"], a["ps"], a["num_stages"], a["k"])
+    hb = plan_hashes(idx, b["cost"], b["status"], b["gap"], b["ps"], b["num_stages"], b["k"])
+    assert torch.equal(ha, hb)
+    sel = torch.arange(0, n, 64, device="cuda")
+    g, c, job = instance("cfg5")
+    ref = oracle.score_batch(staged(g, c, job), plans[sel].cpu().numpy())
+    assert np.array_equal(a["cost"][sel].cpu().numpy().view(np.int64), ref["cost"].view(np.int64))
+    assert np.array_equal(a["status"][sel].cpu().numpy(), ref["status"])
+    assert np.array_equal(a["k"][sel].cpu().numpy(), ref["k"])
+    key = fast.read_argmin(fast.random_argmin_async(pcg, 0, n))
+    cost = a["cost"]
+    m = cost.min()
+    # penalised plans included (ls/baselines.py:275-278); ties -> lexicographically smaller plan
+    ties = torch.nonzero(cost == m)[:, 0].cpu().numpy()
+    best = min(ties, key=lambda i: tuple(plans[i].cpu().tolist()))
+    assert key["cost"] == float(m) and key["evaluated"] == n
+    from paper_2111_10635_b200.search import decode_packed
+    assert list(decode_packed(key["rank"], 4, 64)) == plans[best].cpu().tolist()
