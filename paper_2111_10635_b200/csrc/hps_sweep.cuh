@@ -491,6 +491,14 @@ __device__ double cand_main(const InstanceConsts& c, const WarpSmem<MAXS>& w, Sw
   restricted_prefix<MAXS>(sw, S);
   const double C = c.work / c.batch;
   const int n2 = 2 + sw.pre2[S];
+#ifdef HPS_STATS
+  if (lane == 0) {
+    HPS_STAT(ST_N2, n2);
+    int unc = 0;
+    for (int r = 0; r < S; r++) unc += max(0, sw.kma[r] - sw.blo[r] + 1);
+    HPS_STAT(ST_UNCERT, unc);
+  }
+#endif
   const float fC = (float)C;
   float pl0 = 0.0f;  // sum of pr count(tau_hi)
 #pragma unroll 1

@@ -7,17 +7,21 @@ import sys
 
 
 def parse_disasm(path):
-    secs, cur, loc = {}, None, None
+    secs, cur, loc, fresh = {}, None, None, False
     for line in open(path):
         m = re.match(r"\s*\.text\.(\S+):$", line) or re.match(r"^\.text\.(\S+):", line)
         if m:
             cur = m.group(1); secs[cur] = []; loc = None; continue
         m = re.search(r'//## File "([^"]+)", line (\d+)(.*)', line)
         if m:
-            f = m.group(1).split("/")[-1]
-            inl = re.search(r'inlined at "([^"]+)", line (\d+)', m.group(3))
-            loc = f"{f}:{m.group(2)}" + (f" <- {inl.group(1).split('/')[-1]}:{inl.group(2)}" if inl else "")
+            # a group of comment lines precedes an instruction: the first is the innermost frame
+            if not fresh:
+                f = m.group(1).split("/")[-1]
+                inl = re.search(r'inlined at "([^"]+)", line (\d+)', m.group(3))
+                loc = f"{f}:{m.group(2)}" + (f" <- {inl.group(1).split('/')[-1]}:{inl.group(2)}" if inl else "")
+                fresh = True
             continue
+        fresh = False
         m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
         if m and cur:
             secs[cur].append((m.group(2).strip(), loc))

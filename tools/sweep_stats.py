@@ -9,7 +9,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 NAMES = ["plans", "ideal_survivors", "gen_certified", "cands_eval", "probes_exact", "probes_closed", "cert",
          "cert_fail", "tab", "pending", "stages", "bisect_fallback", "ncand", "plans_fast", "cyc_stages_bisect", "cyc_candidates",
-         "cyc_final", "cyc_pass1", "cyc_pass2"]
+         "cyc_final", "cyc_pass1", "cyc_pass2", "n2_restricted", "n2_uncertified"]
 
 
 def main():
