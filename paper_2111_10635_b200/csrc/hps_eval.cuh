@@ -39,6 +39,24 @@ struct WarpSmem {
   int32_t pre[MAXS + 1];  // exclusive prefix of candidate counts over class leaders
   unsigned long long tsum[kMaxT];
   const TEPair* row[MAXS];  // TE row of stage r's entry (fast path)
+  __device__ __forceinline__ const StageEntry& stage(int r) const { return st[r]; }
+};
+
+// Lean per-warp view of the split path's candidate kernels: the stage entries stay in the
+// (L1-cached, read-only) stage table instead of a 128-byte copy per stage and warp, which leaves
+// the SM's unified L1/shared memory to the threshold-table loads of the exact evaluations.
+template <int MAXS>
+struct WarpSmemL {
+  const StageEntry* sp[MAXS];  // stage-table entry of stage r
+  int32_t kmin[MAXS];   // count at tau_hi
+  int32_t kmax[MAXS];   // count at tau_lo
+  int32_t kres[MAXS];   // final counts
+  int32_t ent[MAXS];
+  int32_t cls[MAXS];
+  int32_t pre[MAXS + 1];
+  unsigned long long tsum[kMaxT];
+  const TEPair* row[MAXS];
+  __device__ __forceinline__ const StageEntry& stage(int r) const { return *sp[r]; }
 };
 
 struct PlanOut {
@@ -909,8 +927,8 @@ __device__ __noinline__ void phase_final(const InstanceConsts& c, const DeviceTa
 // bits): counts at the chosen tau from the tables, add_ps_cores (ls/provisioner.py:486-513) and
 // evaluate()'s monetary cost (ls/costmodel.py:102-167) with per_type_totals in insertion order
 // (ls/domain.py:342-348). One compact out-of-line copy (runs once per plan).
-template <int MAXS>
-__device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, WarpSmem<MAXS>& w, int S, double tau,
+template <int MAXS, class W>
+__device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, W& w, int S, double tau,
                                                  PlanOut& out) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
@@ -919,9 +937,9 @@ __device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, WarpSm
 #pragma unroll 1
   for (int s = lane; s < S; s += 32) {
     const int lo = (int)w.kmin[s], hi = (int)w.kmax[s];
-    const int k = (lo == hi) ? lo : count_seeded(w.st[s], w.row[s], tau, lo, hi);
+    const int k = (lo == hi) ? lo : count_seeded(w.stage(s), w.row[s], tau, lo, hi);
     w.kres[s] = (double)k;
-    const int t = w.st[s].type;
+    const int t = w.stage(s).type;
     if (!c.is_cpu[t]) accel += k;
     if (t == c.ps_type) on_ps += k;
     const double et = __ldg(&w.row[s][k - 1].et);
@@ -951,7 +969,7 @@ __device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, WarpSm
   for (int t = 0; t < c.T; t++) {
     unsigned v = 0;
 #pragma unroll 1
-    for (int s = lane; s < S; s += 32) v += (w.st[s].type == t) ? (unsigned)w.kres[s] : 0u;
+    for (int s = lane; s < S; s += 32) v += (w.stage(s).type == t) ? (unsigned)w.kres[s] : 0u;
     v = __reduce_add_sync(0xffffffffu, v);
     if (lane == 0) w.tsum[t] = v;
   }
@@ -963,7 +981,7 @@ __device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, WarpSm
     bool first = true;
 #pragma unroll 1
     for (int s = 0; s < S; s++) {
-      const int t = w.st[s].type;
+      const int t = w.stage(s).type;
       if (seen >> t & 1u) continue;
       seen |= 1u << t;
       const double term = c.price_s[t] * (double)(w.tsum[t] + (t == c.ps_type ? (unsigned long long)ps : 0ull));

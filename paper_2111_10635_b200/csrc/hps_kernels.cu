@@ -193,8 +193,8 @@ struct Pending {
                              // once per super-chunk, so the list cannot overflow (run_super)
 };
 
-template <int MAXS>
-__device__ __forceinline__ void write_plan(const InstanceConsts& c, const WarpSmem<MAXS>& w,
+template <int MAXS, class W>
+__device__ __forceinline__ void write_plan(const InstanceConsts& c, const W& w,
                                            const Outputs& o, uint64_t p, const PlanOut& r) {
   const int lane = threadIdx.x & 31;
   const bool ok = (r.status & 0x7f) == HPS_ST_OK;
@@ -1125,18 +1125,18 @@ struct PrepState {
 // load PlanState q into the warp's shared-memory view; per-stage constants of the sweep
 template <int MAXS>
 __device__ __forceinline__ void load_state(const InstanceConsts& c, const DeviceTables& tb, const PlanState<MAXS>& ps,
-                                           WarpSmem<MAXS>& w) {
+                                           WarpSmemL<MAXS>& w) {
   const int lane = threadIdx.x & 31;
   const int S = ps.S;
 #pragma unroll 1
   for (int s = lane; s < S; s += 32) {
     const int e = ps.ent[s];
-    const StageEntry st = tb.stages[e];
-    w.st[s] = st;
+    const int type = __ldg(&tb.stages[e].type);
+    w.sp[s] = tb.stages + e;
     w.ent[s] = e;
-    w.row[s] = tb.te + c.te_off[st.type] + (int64_t)(e - st.type * c.P) * (int64_t)(c.et_cap[st.type] + 1);
-    w.kmin[s] = (double)ps.kmin[s];
-    w.kmax[s] = (double)ps.kmax[s];
+    w.row[s] = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
+    w.kmin[s] = ps.kmin[s];
+    w.kmax[s] = ps.kmax[s];
     w.cls[s] = tb_class(tb, e);
   }
   for (int s = lane; s <= S; s += 32) w.pre[s] = ps.pre[s];
@@ -1148,10 +1148,10 @@ template <int MAXS, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, HPS_CAND_MINB / WARPS)
 prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<MAXS>* prep) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
-  SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmem<MAXS>) * WARPS);
+  WarpSmemL<MAXS>* sm = reinterpret_cast<WarpSmemL<MAXS>*>(smem_raw);
+  SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmemL<MAXS>) * WARPS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpSmem<MAXS>& w = sm[warp];
+  WarpSmemL<MAXS>& w = sm[warp];
   SweepSmem<MAXS>& sw = ss[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
@@ -1187,10 +1187,10 @@ __global__ void __launch_bounds__(WARPS * 32, HPS_CAND_MINB / WARPS)
 candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const PrepState<MAXS>* prep, Outputs o,
                  int feasible_only, KeyPart* parts, int first) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
-  SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmem<MAXS>) * WARPS);
+  WarpSmemL<MAXS>* sm = reinterpret_cast<WarpSmemL<MAXS>*>(smem_raw);
+  SweepSmem<MAXS>* ss = reinterpret_cast<SweepSmem<MAXS>*>(smem_raw + sizeof(WarpSmemL<MAXS>) * WARPS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpSmem<MAXS>& w = sm[warp];
+  WarpSmemL<MAXS>& w = sm[warp];
   SweepSmem<MAXS>& sw = ss[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
@@ -1211,7 +1211,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
 #pragma unroll 1
     for (int r = lane; r < S; r += 32) {
       const int lo = ps.kmin[r], hi = ps.kmax[r];
-      sw.pr[r] = c.price_s[w.st[r].type];
+      sw.pr[r] = c.price_s[w.stage(r).type];
       sw.fpr[r] = (float)sw.pr[r];
       sw.kmi[r] = lo;
       sw.kma[r] = hi;
@@ -1314,7 +1314,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(buf + 256 + state_bytes);
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
-  const size_t smem2 = (sizeof(WarpSmem<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
+  const size_t smem2 = (sizeof(WarpSmemL<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
   const size_t smem1 = sizeof(WarpSmem<MAXS>) * WARPS;
   auto kb = bisect_kernel<MAXS, WARPS>;
   CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));

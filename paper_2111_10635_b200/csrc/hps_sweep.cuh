@@ -52,9 +52,9 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
 // threshold table confirms or corrects it (count_verify), so it never affects a result.
 // per-stage FP32 seed constants {rb, 1 - frac, frac} of both sides; a side that cannot decide the
 // count (work 0, frac 0, or dominated per side_dominance) is {0, -1, 0} and contributes q = 0
-template <int MAXS>
-__device__ __forceinline__ void est_setup(const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int r) {
-  const StageEntry& s = w.st[r];
+template <int MAXS, class W>
+__device__ __forceinline__ void est_setup(const W& w, SweepSmem<MAXS>& sw, int r) {
+  const StageEntry& s = w.stage(r);
   const int dom = sw.dom[r];
 #pragma unroll
   for (int side = 0; side < 2; side++) {
@@ -69,8 +69,8 @@ __device__ __forceinline__ void est_setup(const WarpSmem<MAXS>& w, SweepSmem<MAX
 
 // FP32 estimate of count(tau) of unpinned stage r, clamped to [kmin, kmax]. Only a seed: the
 // threshold table confirms or corrects it (count_verify), so it never affects a result.
-template <int MAXS>
-__device__ __forceinline__ int count_est(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r, float tf) {
+template <int MAXS, class W>
+__device__ __forceinline__ int count_est(const W& w, const SweepSmem<MAXS>& sw, int r, float tf) {
   const float* e = sw.est[r];
   const float q0 = e[2] * rcp_approx_f32(tf * e[0] - e[1]);
   const float q1 = e[5] * rcp_approx_f32(tf * e[3] - e[4]);
@@ -90,8 +90,8 @@ __device__ __forceinline__ double te_theta(const TEPair* row, int k) { return __
 // loads pk = {et(k), theta(k - 1)}, thk = theta(k): k is the count iff theta(k) <= tau <
 // theta(k - 1) (count(tau) = min{m : theta(m) <= tau}); otherwise the exact galloping table search
 // from k decides. Returns the count and et at it.
-template <int MAXS>
-__device__ __forceinline__ int count_verify(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int r,
+template <int MAXS, class W>
+__device__ __forceinline__ int count_verify(const W& w, const SweepSmem<MAXS>& sw, int r,
                                             double tau, int k, double2 pk, double thk, double& et) {
   if (thk <= tau && tau < pk.y) {
     et = pk.x;
@@ -111,8 +111,8 @@ struct CostScalars {  // the four job constants the cost needs (no parameter-str
 // one out-of-line copy shared by every call site.
 // gen = (g << 16) | m when tau = et_g(m) and tb.gex certifies count_g(tau) == m: every stage of
 // g's class then has count m and et == tau exactly (the breakpoint value itself).
-template <int MAXS>
-__device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<MAXS>& w,
+template <int MAXS, class W>
+__device__ __noinline__ double cost_exact(const CostScalars cs, const W& w,
                                           const SweepSmem<MAXS>& sw, int S, double tau, int gen) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   const int g = (gen >= 0) ? (gen >> 16) : -1, gm = gen & 0xffff;
@@ -142,8 +142,8 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const WarpSmem<M
 }
 
 // exact cost of one candidate into the lane's tie buffer (one out-of-line copy for every site)
-template <int MAXS>
-__device__ __noinline__ void eval_insert(const CostScalars cs, const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
+template <int MAXS, class W>
+__device__ __noinline__ void eval_insert(const CostScalars cs, const W& w, const SweepSmem<MAXS>& sw,
                                          int S, double tau, int gen, TieBuf& buf) {
   buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau, gen), tau);
 }
@@ -175,8 +175,8 @@ __device__ __forceinline__ int count_lb32(const StageEntry& s, float tau, int do
 
 // candidate i: tau_lo, tau_hi, then the breakpoints et_sp(m) of the class leaders; gen as in
 // cost_exact (-1 unless the leader's breakpoints are certified)
-template <int MAXS>
-__device__ __forceinline__ double cand_tau(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int i,
+template <int MAXS, class W>
+__device__ __forceinline__ double cand_tau(const W& w, const SweepSmem<MAXS>& sw, int i,
                                            int& sp, double tau_lo, double tau_hi, int& gen) {
   gen = -1;
   if (i < 2) return (i == 0) ? tau_lo : tau_hi;
@@ -190,8 +190,8 @@ __device__ __forceinline__ double cand_tau(const WarpSmem<MAXS>& w, const SweepS
 // candidate i of the restricted list: tau_lo, tau_hi, then per class leader sp the certified
 // breakpoints m in [alo, alo + an) (those inside the bound interval) and the uncertified ones
 // m in [blo, kmax]
-template <int MAXS>
-__device__ __forceinline__ double cand_tau2(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int i,
+template <int MAXS, class W>
+__device__ __forceinline__ double cand_tau2(const W& w, const SweepSmem<MAXS>& sw, int i,
                                             int& sp, double tau_lo, double tau_hi, int& gen) {
   gen = -1;
   if (i < 2) return (i == 0) ? tau_lo : tau_hi;
@@ -223,8 +223,8 @@ constexpr int kGrid = HPS_GRID;   // grid points per level of the interval searc
 // E >= tau (certified breakpoint). Each term tau max(kmin, q(1-d) - e) is a max of convex
 // functions of tau (tau q(tau) = (frac/b)(1 + c/(b tau - c)) with c = 1 - frac), so L is convex.
 // Returns L and a subgradient dL/dtau at tau.
-template <int MAXS>
-__device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw, int S, double bo,
+template <int MAXS, class W>
+__device__ __noinline__ void lb_cont(const W& w, const SweepSmem<MAXS>& sw, int S, double bo,
                                         double C, double tau, double& L, double& dL) {
   // kGrid points per level: lanes p, p + kGrid, ... share point p and split its stages,
   // combined by butterfly steps
@@ -233,7 +233,7 @@ __device__ __noinline__ void lb_cont(const WarpSmem<MAXS>& w, const SweepSmem<MA
     const double km = (double)sw.kmi[r];
     double v = km * tau, dv = km;
     if (sw.kma[r] != sw.kmi[r]) {
-      const StageEntry& s = w.st[r];
+      const StageEntry& s = w.stage(r);
 #pragma unroll
       for (int side = 0; side < 2; side++) {
         const double work = side ? s.odt : s.oct;
@@ -295,8 +295,8 @@ __device__ __forceinline__ double grid_point(double ta, double tb) {
 }
 
 // tie buffer overflow (rare): the largest tau of the restricted list whose exact cost is <= lim
-template <int MAXS>
-__device__ __noinline__ double overflow_pass(const CostScalars cs, const WarpSmem<MAXS>& w, const SweepSmem<MAXS>& sw,
+template <int MAXS, class W>
+__device__ __noinline__ double overflow_pass(const CostScalars cs, const W& w, const SweepSmem<MAXS>& sw,
                                              int S, double tau_lo, double tau_hi, int n2, double lim) {
   double bt = -__longlong_as_double(0x7ff0000000000000LL);
   int sp = 0;
@@ -324,20 +324,20 @@ __device__ __noinline__ double overflow_pass(const CostScalars cs, const WarpSme
 // The split path runs them in separate kernels (instruction-cache footprint): part 2 then starts
 // with an empty tie buffer, which loses nothing, because every warm-start candidate that can be
 // the minimum or a tie (cost <= ub + 1e-15) lies in the restricted list and passes the filter.
-template <int MAXS>
-__device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, const WarpSmem<MAXS>& w,
+template <int MAXS, class W>
+__device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, const W& w,
                             SweepSmem<MAXS>& sw, int S, double tau_lo, double tau_hi, int n_cand, TieBuf& buf) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll 1
   for (int r = lane; r < S; r += 32) {
     const bool pinned = (w.kmax[r] == w.kmin[r]);
-    sw.pr[r] = c.price_s[w.st[r].type];
+    sw.pr[r] = c.price_s[w.stage(r).type];
     sw.fpr[r] = (float)sw.pr[r];
     sw.kmi[r] = (int)w.kmin[r];
     sw.kma[r] = (int)w.kmax[r];
     sw.etp[r] = pinned ? w.row[r][(int)w.kmin[r] - 1].et : 0.0;
-    sw.dom[r] = pinned ? 0 : side_dominance(w.st[r], tau_lo, tau_hi, c.bo);
+    sw.dom[r] = pinned ? 0 : side_dominance(w.stage(r), tau_lo, tau_hi, c.bo);
     est_setup<MAXS>(w, sw, r);
     int ld = 0;  // first stage of r's class
     while (w.cls[ld] != w.cls[r]) ld++;
@@ -392,7 +392,7 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
     if (lane < S) {
       const int lo = sw.kmi[lane], chi = min(sw.kma[lane], sw.gex[lane]);
       ok = grid && w.pre[lane + 1] > w.pre[lane] && chi >= lo;
-      if (ok) cstar = min(max(count_seeded(w.st[lane], w.row[lane], tstar, lo, sw.kma[lane]), lo), chi);
+      if (ok) cstar = min(max(count_seeded(w.stage(lane), w.row[lane], tstar, lo, sw.kma[lane]), lo), chi);
     }
     const unsigned lm = __ballot_sync(0xffffffffu, ok);
     const int nl = __popc(lm);
@@ -440,8 +440,8 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
         int alo = 0, an = 0;
         const int chi = min(hi, sw.gex[r]);   // certified part [lo, chi]
         if (ta <= tbh && chi >= lo) {
-          const int ma = count_seeded(w.st[r], w.row[r], tbh, lo, hi);  // smallest certified m
-          const int mb = count_seeded(w.st[r], w.row[r], ta, lo, hi);   // largest certified m
+          const int ma = count_seeded(w.stage(r), w.row[r], tbh, lo, hi);  // smallest certified m
+          const int mb = count_seeded(w.stage(r), w.row[r], ta, lo, hi);   // largest certified m
           alo = max(ma, lo);
           an = max(0, min(mb, chi) - alo + 1);
         }
@@ -482,8 +482,8 @@ __device__ __forceinline__ void restricted_prefix(SweepSmem<MAXS>& sw, int S) {
   __syncwarp();
 }
 
-template <int MAXS>
-__device__ double cand_main(const InstanceConsts& c, const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
+template <int MAXS, class W>
+__device__ double cand_main(const InstanceConsts& c, const W& w, SweepSmem<MAXS>& sw, int S,
                             double tau_lo, double tau_hi, double ub, TieBuf& buf) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
@@ -531,7 +531,7 @@ __device__ double cand_main(const InstanceConsts& c, const WarpSmem<MAXS>& w, Sw
         for (int q = 0; q < kTop; q++) {
           const int r = top[q];
           if (r < 0 || r == g) continue;
-          const int d = count_lb32(w.st[r], tf, sw.dom[r]) - sw.kmi[r];
+          const int d = count_lb32(w.stage(r), tf, sw.dom[r]) - sw.kmi[r];
           if (d > 0) P += sw.fpr[r] * (float)d;
         }
         keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > ub + 1e-15);
@@ -570,9 +570,9 @@ __device__ double cand_main(const InstanceConsts& c, const WarpSmem<MAXS>& w, Sw
   return warp_max(bt);
 }
 
-template <int MAXS>
+template <int MAXS, class W>
 __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTables& tb,
-                                        const WarpSmem<MAXS>& w, SweepSmem<MAXS>& sw, int S,
+                                        const W& w, SweepSmem<MAXS>& sw, int S,
                                         double tau_lo, double tau_hi, int n_cand) {
   TieBuf buf;
   buf.init();
@@ -581,8 +581,8 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
 }
 
 // Whole plan, fast path. Falls back to the literal path's pending marker for >4096 candidates.
-template <int MAXS>
-__device__ void eval_plan_fast(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
+template <int MAXS, class W>
+__device__ void eval_plan_fast(const InstanceConsts& c, const DeviceTables& tb, W& w,
                                SweepSmem<MAXS>& sw, int d0, int d1, PlanOut& out) {
   out.ps = 0;
   out.gap = 0.0;
