@@ -19,6 +19,8 @@ Side measurements on the other BASELINE configs (keys of the same JSON line):
          per-round CUDA events, and the public train() call timed up to the best round
   cfg1   RL 200 rounds x 64 plans, seeds 0-2, public train() wall time per seed
   cfg2   exhaustive 3^8 brute force through the public brute_force() (wall, host result)
+  enum_pruned  the cfg3 search with certified subtree pruning (same winner; not a plans-evaluated
+         rate: 3^16 / wall time of the whole pruned search)
 
 `--impl reference` times the CPU oracle (oracle/, the C restatement of the reference's path;
 the reference itself is Python and has no compiled form) on all host cores over a strided
@@ -505,7 +507,7 @@ def run_ours(args):
         rl = measure_rl(torch, *instance("cfg4"))
         if not args.no_small:
             cfg1 = measure_cfg1(torch)
-    if not args.no_small and rank == 0:
+    if not args.no_small and world == 1:   # brute_force would all_gather across ranks
         cfg2 = measure_cfg2(torch)
     r5 = None
     if not args.no_cfg5:

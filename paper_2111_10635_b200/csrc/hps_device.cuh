@@ -3,6 +3,7 @@
 // rounds exactly like CPython/numpy binary64 (the bit-exact contract of SURVEY.md §7).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "../../include/hps.h"
@@ -27,6 +28,24 @@ __device__ unsigned long long g_stats[24];
 #define HPS_STAT(i, v) atomicAdd(&hps::g_stats[i], (unsigned long long)(v))
 #else
 #define HPS_STAT(i, v) ((void)0)
+#endif
+
+// Bounds-checked build (-DHPS_CHECKS, `make checked`): every threshold-table access and the
+// per-warp / pending-list indices below trap with a message when out of range. The tests run
+// against that build on the GPU box in place of compute-sanitizer (closed on this pool).
+#ifdef HPS_CHECKS
+__device__ const char* g_chk_te_lo;   // [lo, hi) of the threshold table of the running launch
+__device__ const char* g_chk_te_hi;
+#define HPS_CHECK(cond, what)                                                                  \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("HPS_CHECK failed: %s at %s:%d (block %d thread %d)\n", what, __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)threadIdx.x);                                               \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define HPS_CHECK(cond, what) ((void)0)
 #endif
 
 constexpr int kMaxL = HPS_MAX_LAYERS;
@@ -176,6 +195,16 @@ struct __align__(16) TEPair {
   double et;
   double th;  // theta(m - 1)
 };
+
+// checked element access of a threshold-table row (plain indexing in the product build)
+__device__ __forceinline__ const TEPair& te_checked(const TEPair* row, long i) {
+#ifdef HPS_CHECKS
+  const char* p = reinterpret_cast<const char*>(row + i);
+  HPS_CHECK(p >= g_chk_te_lo && p + sizeof(TEPair) <= g_chk_te_hi, "threshold-table index out of range");
+#endif
+  return row[i];
+}
+#define HPS_TE(row, i) (::hps::te_checked((row), (i)))
 
 // Stage-0 exits of optimize_k1 for an entry starting at layer 0 (ls/provisioner.py:394-397)
 struct Stage0Info {

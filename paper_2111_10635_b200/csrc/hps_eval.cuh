@@ -142,25 +142,25 @@ static __device__ HPS_NOINLINE_RARE int count_tab(const TEPair* row, double tau,
   if (lo >= hi) return lo;
   HPS_STAT(ST_TAB, 1);
   const int m = min(max(g, lo), hi);
-  if (row[m].th <= tau) {  // count <= m: gallop down
+  if (HPS_TE(row, m).th <= tau) {  // count <= m: gallop down
     int hb = m, lb, step = 1;
     for (;;) {
       const int cnd = hb - step;
       if (cnd < lo) { lb = lo - 1; break; }
-      if (row[cnd].th <= tau) { hb = cnd; step <<= 1; } else { lb = cnd; break; }
+      if (HPS_TE(row, cnd).th <= tau) { hb = cnd; step <<= 1; } else { lb = cnd; break; }
     }
-    while (hb - lb > 1) { const int md = (lb + hb) >> 1; if (row[md].th <= tau) hb = md; else lb = md; }
+    while (hb - lb > 1) { const int md = (lb + hb) >> 1; if (HPS_TE(row, md).th <= tau) hb = md; else lb = md; }
     return hb;
   }
   int lb = m, hb, step = 1;  // count > m: gallop up (count <= hi is guaranteed)
   for (;;) {
     const int cnd = lb + step;
     if (cnd >= hi) { hb = hi; break; }
-    if (row[cnd].th <= tau) { hb = cnd; break; }
+    if (HPS_TE(row, cnd).th <= tau) { hb = cnd; break; }
     lb = cnd;
     step <<= 1;
   }
-  while (hb - lb > 1) { const int md = (lb + hb) >> 1; if (row[md].th <= tau) hb = md; else lb = md; }
+  while (hb - lb > 1) { const int md = (lb + hb) >> 1; if (HPS_TE(row, md).th <= tau) hb = md; else lb = md; }
   return hb;
 }
 
@@ -248,7 +248,7 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
             const bool mine = (slot ? u1 : u0) && ty[slot] == t;
             if (mine) {
               const long long K = c.quota[t] - (sum_b - lb[slot]);  // >= lb (quota_ok(b))
-              th = fmax(th, row[slot][(int)K].th);                  // count <= K <=> tau >= theta(K)
+              th = fmax(th, HPS_TE(row[slot], (int)K).th);                  // count <= K <=> tau >= theta(K)
             }
           }
         }
@@ -367,8 +367,8 @@ static __device__ __noinline__ int count_seeded(const StageEntry& s, const TEPai
   }
   int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
   k = min(max(k, lo), hi);
-  const double2 pk = __ldg(reinterpret_cast<const double2*>(row + (k - 1)));  // {et(k), theta(k-1)}
-  const double thk = __ldg(&row[k].th);
+  const double2 pk = __ldg(reinterpret_cast<const double2*>(&HPS_TE(row, k - 1)));  // {et(k), theta(k-1)}
+  const double thk = __ldg(&HPS_TE(row, k).th);
   if (thk <= tau && tau < pk.y) return k;
   return count_tab(row, tau, lo, hi, k);
 }
@@ -429,7 +429,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
     double lt = -inf;
 #pragma unroll
     for (int slot = 0; slot < 2; slot++)
-      if (mb[slot]) lt = fmax(lt, __ldg(&row[slot][Q].th));
+      if (mb[slot]) lt = fmax(lt, __ldg(&HPS_TE(row[slot], Q).th));
     lt = warp_max(lt);
     // exact counts at L_t (each <= Q there): when their sum is within the quota, tau*_t = L_t
     int cnt[2] = {0, 0};
@@ -502,7 +502,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
           const int k = ++cnt[sl];
           double v = -inf;
           if (k < Q) {
-            v = __ldg(&row[sl][k].th);
+            v = __ldg(&HPS_TE(row[sl], k).th);
             if (!(v >= lt)) v = -inf;
           }
           nx[sl] = v;
@@ -528,7 +528,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
         if (lane == __ffs(own) - 1) {
           const int sl = (nx[0] == e) ? 0 : 1;
           const int k = --cnt[sl];
-          nx[sl] = (k > kb[sl]) ? __ldg(&row[sl][k - 1].th) : inf;
+          nx[sl] = (k > kb[sl]) ? __ldg(&HPS_TE(row[sl], k - 1).th) : inf;
         }
       }
     }
@@ -664,6 +664,7 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
   const int c0 = __popc(m0);
   const int S = c0 + __popc(m1);
   out.S = S;
+  HPS_CHECK(S <= MAXS, "more stages than the warp view holds");
   // lane s builds stage s and s+32
   bool invalid = false;
   for (int slot = 0; slot < 2; slot++) {
@@ -942,7 +943,7 @@ __device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, W& w, 
     const int t = w.stage(s).type;
     if (!c.is_cpu[t]) accel += k;
     if (t == c.ps_type) on_ps += k;
-    const double et = __ldg(&w.row[s][k - 1].et);
+    const double et = __ldg(&HPS_TE(w.row[s], k - 1).et);
     emax = (et > emax) ? et : emax;
   }
   accel = (int)__reduce_add_sync(0xffffffffu, (unsigned)accel);

@@ -249,6 +249,7 @@ eval_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       if (lane == 0) {
         HPS_STAT(ST_PENDING, 1);
         unsigned int at = atomicAdd(pend.count, 1u);
+        HPS_CHECK(at < pend.cap, "pending list overflow");
         if (at < pend.cap) pend.list[at] = p;
       }
     } else if (!ARGMIN) {
@@ -524,6 +525,7 @@ slow_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src,
       const int nraw = s_ncand;
       int npow = 1;
       while (npow < nraw) npow <<= 1;
+      HPS_CHECK((size_t)npow <= per_block / 2, "slow-path sort buffer too small");
       const double inf = __longlong_as_double(0x7ff0000000000000LL);
       // raw candidates: tau_lo, tau_hi, then each class leader's breakpoints et(m) for m from
       // kmax down to kmin (ascending: et is non-increasing in m); values below tau_lo become
@@ -928,8 +930,8 @@ __global__ void gen_exact_kernel(const InstanceConsts c, const TEPair* te, int32
   const int64_t pe = idx / cap;
   const int m = (int)(idx % cap) + 1;
   const TEPair* row = te + c.te_off[t] + pe * (cap + 1);
-  const double et = row[m - 1].et;  // et(m); row[m - 1].th = theta(m - 1), row[m].th = theta(m)
-  if (!((row[m].th <= et) && (et < row[m - 1].th))) atomicMin(gex + t * c.P + pe, m - 1);
+  const double et = HPS_TE(row, m - 1).et;  // et(m); row[m - 1].th = theta(m - 1), row[m].th = theta(m)
+  if (!((HPS_TE(row, m).th <= et) && (et < HPS_TE(row, m - 1).th))) atomicMin(gex + t * c.P + pe, m - 1);
 }
 
 }  // namespace
@@ -949,11 +951,30 @@ struct HpsInstance {
   int sm_count = 148;
   int grid_per_sm = 16;   // blocks per SM of the split kernels' grid (HPS_GRID_PER_SM)
   int carveout = -1;      // shared-memory carveout % for the split kernels (HPS_CARVEOUT)
+  size_t te_bytes = 0;    // threshold-table size (bounds of the checked build)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
 };
 
 namespace {
+
+// checked build: the threshold-table range the kernels of this stream may touch
+int chk_bind(const HpsInstance* in, cudaStream_t st) {
+#ifdef HPS_CHECKS
+  // (a captured copy would read this host stack at replay: graph captures keep the binding of
+  // the eager call that precedes them)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return HPS_OK;
+  const char* lo = reinterpret_cast<const char*>(in->d_te);
+  const char* hi = lo + in->te_bytes;
+  CUDA_TRY(cudaMemcpyToSymbolAsync(g_chk_te_lo, &lo, sizeof(lo), 0, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyToSymbolAsync(g_chk_te_hi, &hi, sizeof(hi), 0, cudaMemcpyHostToDevice, st));
+#else
+  (void)in; (void)st;
+#endif
+  return HPS_OK;
+}
 
 // ------------------------------------------------------------------ split fast path
 // K1a: runs, exits and the quota bisection; finished (infeasible) plans are emitted here, the
@@ -973,6 +994,7 @@ struct PlanState {
 struct Cont {
   void* states;
   unsigned int* count;
+  unsigned int cap;   // PlanState slots (the chunk size)
 };
 
 __device__ __forceinline__ void merge_part(KeyPart* parts, uint64_t slot, int first, const Key& best,
@@ -1022,6 +1044,7 @@ stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src
       unsigned int at = 0;
       if (lane == 0) at = atomicAdd(cont.count, 1u);
       at = __shfl_sync(0xffffffffu, at, 0);
+      HPS_CHECK(at < cont.cap, "plan-state chunk overflow");
       PlanState<MAXS>& ps = states[at];
       for (int s = lane; s < r.S; s += 32) {
         ps.ent[s] = w.ent[s];
@@ -1098,6 +1121,7 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
       if (lane == 0) {
         HPS_STAT(ST_PENDING, 1);
         const unsigned int at = atomicAdd(pend.count, 1u);
+        HPS_CHECK(at < pend.cap, "pending list overflow");
         if (at < pend.cap) pend.list[at] = ps.p;
         ps.n_cand = -1;
       }
@@ -1215,7 +1239,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
       sw.fpr[r] = (float)sw.pr[r];
       sw.kmi[r] = lo;
       sw.kma[r] = hi;
-      sw.etp[r] = (lo == hi) ? __ldg(&w.row[r][lo - 1].et) : 0.0;
+      sw.etp[r] = (lo == hi) ? __ldg(&HPS_TE(w.row[r], lo - 1).et) : 0.0;
       sw.dom[r] = pp.dom[r];
       est_setup<MAXS>(w, sw, r);
       sw.lead[r] = pp.lead[r];
@@ -1310,7 +1334,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   char* buf = nullptr;
   const size_t state_bytes = (sizeof(PlanState<MAXS>) * chunk + 255) / 256 * 256;
   CUDA_TRY(cudaMallocAsync(&buf, state_bytes + sizeof(PrepState<MAXS>) * chunk + 256, st));
-  Cont cont{buf + 256, reinterpret_cast<unsigned int*>(buf)};
+  Cont cont{buf + 256, reinterpret_cast<unsigned int*>(buf), (unsigned int)chunk};
   PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(buf + 256 + state_bytes);
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
@@ -1438,6 +1462,7 @@ int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_onl
     CUDA_TRY(cudaGetLastError());
     return HPS_OK;
   }
+  if (int rc = chk_bind(in, st)) return rc;
   const uint64_t sc = in->super_chunk;
   const uint64_t nsc = (n + sc - 1) / sc;
   const uint64_t n0 = std::min(n, sc);
@@ -1591,6 +1616,8 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   CUDA_TRY(cudaMalloc(&in->d_stages, sizeof(StageEntry) * ne));
   CUDA_TRY(cudaMalloc(&in->d_stage0, sizeof(Stage0Info) * T * L));
   CUDA_TRY(cudaMalloc(&in->d_te, sizeof(TEPair) * off));
+  in->te_bytes = sizeof(TEPair) * off;
+  if (int rc = chk_bind(in, 0)) return rc;
   CUDA_TRY(cudaMalloc(&in->d_cls, sizeof(int32_t) * ne));
   CUDA_TRY(cudaMalloc(&in->d_gex, sizeof(int32_t) * ne));
   HPS_COUNT_LAUNCH();
@@ -1669,6 +1696,7 @@ int hps_score_plans(HpsInstance* in, const uint8_t* d_plans, int64_t n, const Hp
   src.mode = 0;
   src.plans = d_plans;
   // super-chunks as in argmin_common: the pending list holds a whole chunk
+  if (int rc = chk_bind(in, st)) return rc;
   const uint64_t sc = in->super_chunk;
   const uint64_t cap = std::min<uint64_t>((uint64_t)n, sc);
   char* buf = nullptr;

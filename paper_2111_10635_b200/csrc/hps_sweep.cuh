@@ -46,6 +46,9 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   int32_t gex[MAXS]; // leader r: count_r(et_r(m)) == m for m <= gex[r] (tb.gex), else 0
   double q[64];      // survivors of the lower-bound filter, evaluated 32 at a time
   int32_t qg[64];    // their generator: (leader << 16) | m, or -1 (tau_lo / tau_hi)
+  double p0;         // sum over pinned stages of pr * count (the bound's linear part)
+  int32_t nu;        // unpinned stages, in stage order:
+  int8_t ulist[MAXS];
 };
 
 // FP32 estimate of count(tau) of unpinned stage r, clamped to [kmin, kmax]. Only a seed: the
@@ -82,9 +85,9 @@ __device__ __forceinline__ int count_est(const W& w, const SweepSmem<MAXS>& sw, 
 
 // read-only table loads: {et(k), theta(k - 1)} in one 16-byte load, theta(k) separately
 __device__ __forceinline__ double2 te_pair(const TEPair* row, int k) {
-  return __ldg(reinterpret_cast<const double2*>(row + (k - 1)));
+  return __ldg(reinterpret_cast<const double2*>(&HPS_TE(row, k - 1)));
 }
-__device__ __forceinline__ double te_theta(const TEPair* row, int k) { return __ldg(&row[k].th); }
+__device__ __forceinline__ double te_theta(const TEPair* row, int k) { return __ldg(&HPS_TE(row, k).th); }
 
 // Exact count(tau) for tau in [tau_lo, tau_hi] (count in [kmin, kmax]) given the seed k and the
 // loads pk = {et(k), theta(k - 1)}, thk = theta(k): k is the count iff theta(k) <= tau <
@@ -99,7 +102,7 @@ __device__ __forceinline__ int count_verify(const W& w, const SweepSmem<MAXS>& s
   }
   const TEPair* row = w.row[r];
   k = count_tab(row, tau, sw.kmi[r], sw.kma[r], k);
-  et = __ldg(&row[k - 1].et);
+  et = __ldg(&HPS_TE(row, k - 1).et);
   return k;
 }
 
@@ -184,7 +187,7 @@ __device__ __forceinline__ double cand_tau(const W& w, const SweepSmem<MAXS>& sw
   while (w.pre[sp + 1] <= j) sp++;
   const int m = (int)w.kmin[sp] + (j - w.pre[sp]);
   if (m <= sw.gex[sp]) gen = (sp << 16) | m;
-  return __ldg(&w.row[sp][m - 1].et);
+  return __ldg(&HPS_TE(w.row[sp], m - 1).et);
 }
 
 // candidate i of the restricted list: tau_lo, tau_hi, then per class leader sp the certified
@@ -205,7 +208,7 @@ __device__ __forceinline__ double cand_tau2(const W& w, const SweepSmem<MAXS>& s
   } else {
     m = sw.blo[sp] + (o - sw.an[sp]);
   }
-  return __ldg(&w.row[sp][m - 1].et);
+  return __ldg(&HPS_TE(w.row[sp], m - 1).et);
 }
 
 #ifndef HPS_GRID
@@ -226,28 +229,31 @@ constexpr int kGrid = HPS_GRID;   // grid points per level of the interval searc
 template <int MAXS, class W>
 __device__ __noinline__ void lb_cont(const W& w, const SweepSmem<MAXS>& sw, int S, double bo,
                                         double C, double tau, double& L, double& dL) {
-  // kGrid points per level: lanes p, p + kGrid, ... share point p and split its stages,
-  // combined by butterfly steps
-  double P = 0.0, dP = 0.0;
-  for (int r = (threadIdx.x & 31) / kGrid; r < S; r += 32 / kGrid) {
+  // kGrid points per level: lanes p, p + kGrid, ... share point p and split the unpinned stages,
+  // combined by butterfly steps; pinned stages contribute tau * p0 (slope p0), counted once.
+  // A stage whose count one side decides on [tau_lo, tau_hi] (side_dominance) uses that side.
+  const int grp = (threadIdx.x & 31) / kGrid;
+  double P = (grp == 0) ? tau * sw.p0 : 0.0, dP = (grp == 0) ? sw.p0 : 0.0;
+  for (int j = grp; j < sw.nu; j += 32 / kGrid) {
+    const int r = sw.ulist[j];
+    const int dom = sw.dom[r];
     const double km = (double)sw.kmi[r];
     double v = km * tau, dv = km;
-    if (sw.kma[r] != sw.kmi[r]) {
-      const StageEntry& s = w.stage(r);
+    const StageEntry& s = w.stage(r);
 #pragma unroll
-      for (int side = 0; side < 2; side++) {
-        const double work = side ? s.odt : s.oct;
-        const double frac = side ? s.beta : s.alpha;
-        if (work == 0.0 || frac == 0.0) continue;
-        const double cc = side ? s.omb : s.oma;
-        const double h = tau * (bo * (side ? s.rwd : s.rwo)) - cc;
-        if (!(h > 0.0)) { v = __longlong_as_double(0x7ff0000000000000LL); dv = 0.0; continue; }
-        const double rh = rcp_1nt(h);
-        const double q = frac * rh;
-        const double vq = tau * (q * (1.0 - 1e-8) - 1e-9);
-        // d(tau q)/dtau = -q^2 c / frac = -q c / h
-        if (vq > v) { v = vq; dv = (1.0 - 1e-8) * (-q * cc * rh) - 1e-9; }
-      }
+    for (int side = 0; side < 2; side++) {
+      if (dom == 2 - side) continue;
+      const double work = side ? s.odt : s.oct;
+      const double frac = side ? s.beta : s.alpha;
+      if (work == 0.0 || frac == 0.0) continue;
+      const double cc = side ? s.omb : s.oma;
+      const double h = tau * (bo * (side ? s.rwd : s.rwo)) - cc;
+      if (!(h > 0.0)) { v = __longlong_as_double(0x7ff0000000000000LL); dv = 0.0; continue; }
+      const double rh = rcp_1nt(h);
+      const double q = frac * rh;
+      const double vq = tau * (q * (1.0 - 1e-8) - 1e-9);
+      // d(tau q)/dtau = -q^2 c / frac = -q c / h
+      if (vq > v) { v = vq; dv = (1.0 - 1e-8) * (-q * cc * rh) - 1e-9; }
     }
     P += sw.pr[r] * v;
     dP += sw.pr[r] * dv;
@@ -259,7 +265,6 @@ __device__ __noinline__ void lb_cont(const W& w, const SweepSmem<MAXS>& sw, int 
   L = C * P;
   dL = C * dP;
 }
-
 
 // One level of the interval search: lane j < 16 holds (t, L, dL) at grid point j of [ta, tb]
 // (point 15 = tb). On each cell, convexity bounds L from below by max(tangent at the left end, tangent
@@ -344,6 +349,21 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
     sw.lead[r] = (int8_t)ld;
     sw.gex[r] = (ld == r && !pinned) ? __ldg(tb.gex + w.ent[r]) : 0;
   }
+  {  // unpinned stages in order, and the pinned stages' part of the bound
+    double p0 = 0.0;
+    int base = 0;
+#pragma unroll
+    for (int slot = 0; slot < 2; slot++) {
+      const int r = lane + 32 * slot;
+      const bool unp = r < S && w.kmax[r] != w.kmin[r];
+      if (r < S && !unp) p0 += c.price_s[w.stage(r).type] * w.kmin[r];
+      const unsigned m = __ballot_sync(0xffffffffu, unp);
+      if (unp) sw.ulist[base + __popc(m & ((1u << lane) - 1u))] = (int8_t)r;
+      base += __popc(m);
+    }
+    for (int o = 16; o; o >>= 1) p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+    if (lane == 0) { sw.nu = base; sw.p0 = p0; }
+  }
   __syncwarp();
   if (lane == 0) {
     int t[kTop > 0 ? kTop : 1];
@@ -406,7 +426,7 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
       const int m = cr + off;
       if (r < S && m >= sw.kmi[r] && m <= min(sw.kma[r], sw.gex[r])) {
         gen = (r << 16) | m;
-        tau = __ldg(&w.row[r][m - 1].et);
+        tau = __ldg(&HPS_TE(w.row[r], m - 1).et);
       }
     } else {
       const int i = (int)(((long long)lane * n_cand) >> 5);
