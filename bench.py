@@ -429,9 +429,19 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        # NCCL_DEBUG stays the caller's; NCCL's own log goes to stderr so stdout keeps ONE JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL_DEBUG stays the caller's (the image sets VERSION). NCCL prints its banner on fd 1
+        # while the communicator is created: fd 1 points at stderr for that window, so stdout
+        # keeps exactly one JSON line and the NCCL lines stay in the log.
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     g, c, job = instance()
