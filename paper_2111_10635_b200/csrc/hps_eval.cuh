@@ -40,6 +40,7 @@ struct WarpSmem {
   unsigned long long tsum[kMaxT];
   const TEPair* row[MAXS];  // TE row of stage r's entry (fast path)
   __device__ __forceinline__ const StageEntry& stage(int r) const { return st[r]; }
+  __device__ __forceinline__ void bind(int r, const StageEntry* e) { st[r] = *e; }
 };
 
 // Lean per-warp view of the split path's candidate kernels: the stage entries stay in the
@@ -50,13 +51,14 @@ struct WarpSmemL {
   const StageEntry* sp[MAXS];  // stage-table entry of stage r
   int32_t kmin[MAXS];   // count at tau_hi
   int32_t kmax[MAXS];   // count at tau_lo
-  int32_t kres[MAXS];   // final counts
+  double kres[MAXS];    // final counts (Python ints: the quota-gap path can see huge ones)
   int32_t ent[MAXS];
   int32_t cls[MAXS];
   int32_t pre[MAXS + 1];
   unsigned long long tsum[kMaxT];
   const TEPair* row[MAXS];
   __device__ __forceinline__ const StageEntry& stage(int r) const { return *sp[r]; }
+  __device__ __forceinline__ void bind(int r, const StageEntry* e) { sp[r] = e; }
 };
 
 struct PlanOut {
@@ -180,9 +182,9 @@ __device__ __forceinline__ bool quota_sums_ok(const InstanceConsts& c, unsigned 
 
 // Bisection on quota_ok (ls/provisioner.py:430-437). Inputs: counts at tau_hi in kb[] (finite,
 // quota-feasible). Output: tau_lo and the counts at tau_lo.
-static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, const StageEntry* st,
-                              const int32_t* ent, int S, double a, double b, const double kb_in[2],
-                              int kb_out[2]) {
+template <class W>
+__device__ __forceinline__ double bisect_fast(const InstanceConsts& c, const DeviceTables& tb, const W& w,
+                                              int S, double a, double b, const double kb_in[2], int kb_out[2]) {
   const int lane = threadIdx.x & 31;
   int lb[2], ub[2], ty[2] = {-1, -1}, Q[2] = {0, 0};
   const TEPair* row[2] = {nullptr, nullptr};
@@ -192,9 +194,9 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
     const int s = lane + 32 * slot;
     lb[slot] = ub[slot] = 0;
     if (s < S) {
-      ty[slot] = st[s].type;
+      ty[slot] = w.stage(s).type;
       Q[slot] = (int)c.quota[ty[slot]];
-      row[slot] = te_row(c, tb, ty[slot], ent[s]);
+      row[slot] = te_row(c, tb, ty[slot], w.ent[s]);
       lb[slot] = (int)kb_in[slot];
       ub[slot] = kOver;
       thq[slot] = row[slot][Q[slot]].th;  // count <= Q  <=>  tau >= theta(Q)
@@ -281,8 +283,8 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
         } else {
           const int s = lane + 32 * slot;
           const int hi = (ub[slot] == kOver) ? Q[slot] : ub[slot];
-          const int kc = count_cert(st[s], mid, c.bo);  // mid >= theta(Q): no raise here
-          km[slot] = (kc >= lb[slot] && kc <= hi) ? kc : count_tab(row[slot], mid, lb[slot], hi, est_count(st[s], mid));
+          const int kc = count_cert(w.stage(s), mid, c.bo);  // mid >= theta(Q): no raise here
+          km[slot] = (kc >= lb[slot] && kc <= hi) ? kc : count_tab(row[slot], mid, lb[slot], hi, est_count(w.stage(s), mid));
         }
       }
     }
@@ -303,9 +305,9 @@ static __device__ HPS_NOINLINE double bisect_fast(const InstanceConsts& c, const
     for (int slot = 0; slot < 2; slot++)
       if (ty[slot] >= 0 && ub[slot] != lb[slot]) {
         const int hi = (ub[slot] == kOver) ? Q[slot] : ub[slot];
-        const int kc = count_cert(st[lane + 32 * slot], b, c.bo);
+        const int kc = count_cert(w.stage(lane + 32 * slot), b, c.bo);
         lb[slot] = (kc >= lb[slot] && kc <= hi) ? kc
-                                                 : count_tab(row[slot], b, lb[slot], hi, est_count(st[lane + 32 * slot], b));
+                                                 : count_tab(row[slot], b, lb[slot], hi, est_count(w.stage(lane + 32 * slot), b));
       }
   } else if (it < 60) {
     // every unpinned stage has count(a) == count(b) + 1 (or "over" with count(b) == Q):
@@ -403,9 +405,10 @@ __device__ __forceinline__ float q_cont(const StageEntry& s, float tau, float& d
 // counts at the final b (= tau_lo) are read from the tables. Mids in (serial, tau_hi) never
 // raise in _floor_count except where counts exceed every quota (mid < L_t), where quota_ok is
 // false either way.
-static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, const StageEntry* st,
-                                                    const TEPair* const* rows, int S, double a, double b,
-                                                    const double kb_in[2], int kb_out[2]) {
+template <class W>
+__device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W& w, int S, double a, double b,
+                                                const double kb_in[2], int kb_out[2]) {
+  const TEPair* const* rows = w.row;
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   int ty[2], kb[2];
@@ -413,7 +416,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
 #pragma unroll
   for (int slot = 0; slot < 2; slot++) {
     const int s = lane + 32 * slot;
-    ty[slot] = (s < S) ? st[s].type : -1;
+    ty[slot] = (s < S) ? w.stage(s).type : -1;
     kb[slot] = (s < S) ? (int)kb_in[slot] : 0;
     row[slot] = (s < S) ? rows[s] : nullptr;
   }
@@ -435,7 +438,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
     int cnt[2] = {0, 0};
 #pragma unroll
     for (int slot = 0; slot < 2; slot++)
-      if (mb[slot]) cnt[slot] = count_seeded(st[lane + 32 * slot], row[slot], lt, kb[slot], Q);
+      if (mb[slot]) cnt[slot] = count_seeded(w.stage(lane + 32 * slot), row[slot], lt, kb[slot], Q);
     const int sl = (int)__reduce_add_sync(0xffffffffu, (unsigned)(cnt[0] + cnt[1]));
     if (sl <= Q) {
       tstar = fmax(tstar, lt);
@@ -454,7 +457,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
       for (int slot = 0; slot < 2; slot++)
         if (mb[slot]) {
           float d;
-          F += q_cont(st[lane + 32 * slot], x, d);
+          F += q_cont(w.stage(lane + 32 * slot), x, d);
           dF += d;
         }
       for (int o = 16; o; o >>= 1) {
@@ -472,7 +475,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
     // ---- exact counts at te and exact selection of tau*_t ----
 #pragma unroll
     for (int slot = 0; slot < 2; slot++)
-      if (mb[slot]) cnt[slot] = count_seeded(st[lane + 32 * slot], row[slot], te, kb[slot], Q);
+      if (mb[slot]) cnt[slot] = count_seeded(w.stage(lane + 32 * slot), row[slot], te, kb[slot], Q);
     const int se = (int)__reduce_add_sync(0xffffffffu, (unsigned)(cnt[0] + cnt[1]));
     double tt;
     if (se <= Q) {
@@ -541,7 +544,7 @@ static __device__ HPS_NOINLINE double bisect_direct(const InstanceConsts& c, con
   }
 #pragma unroll
   for (int slot = 0; slot < 2; slot++)
-    kb_out[slot] = (ty[slot] >= 0) ? count_seeded(st[lane + 32 * slot], row[slot], b, kb[slot], (int)c.quota[ty[slot]])
+    kb_out[slot] = (ty[slot] >= 0) ? count_seeded(w.stage(lane + 32 * slot), row[slot], b, kb[slot], (int)c.quota[ty[slot]])
                                    : kb[slot];
   return b;
 }
@@ -553,7 +556,7 @@ __device__ __forceinline__ double candidate_cost(const InstanceConsts& c, const 
                                                  const WarpSmem<MAXS>& w, int S, double tau) {
   double E = 0.0, P = 0.0;
   for (int r = 0; r < S; r++) {
-    const StageEntry& s = w.st[r];
+    const StageEntry& s = w.stage(r);
     double k = w.kmin[r];
     if (w.kmax[r] != k) {
       const int kc = CERT ? count_cert(s, tau, c.bo) : -1;
@@ -573,8 +576,8 @@ __device__ __forceinline__ double candidate_cost(const InstanceConsts& c, const 
 // slots), then the candidate count over class leaders (identical (oct, odt, alpha, beta) =>
 // identical counts and breakpoints, so only the first stage of a class contributes distinct
 // values) and its exclusive prefix in w.pre; n_cand includes tau_lo and tau_hi.
-template <int MAXS>
-__device__ __forceinline__ void cands_prefix(const DeviceTables& tb, WarpSmem<MAXS>& w, int S, const double kb[2],
+template <int MAXS, class W>
+__device__ __forceinline__ void cands_prefix(const DeviceTables& tb, W& w, int S, const double kb[2],
                                              int& n_cand) {
   const int lane = threadIdx.x & 31;
   for (int slot = 0; slot < 2; slot++) {
@@ -612,8 +615,8 @@ __device__ __forceinline__ void cands_prefix(const DeviceTables& tb, WarpSmem<MA
 
 // Fast-path bisection from the counts at tau_hi (w.kmin) on (serial, tau_hi), then the candidate
 // prefix. Needs w.st, w.ent, w.row, w.kmin.
-template <int MAXS>
-__device__ __forceinline__ void phase_bisect_cands(const InstanceConsts& c, const DeviceTables& tb, WarpSmem<MAXS>& w,
+template <int MAXS, class W>
+__device__ __forceinline__ void phase_bisect_cands(const InstanceConsts& c, const DeviceTables& tb, W& w,
                                                    int S, double a, double b, double& tau_lo_out, int& n_cand) {
   const int lane = threadIdx.x & 31;
   double kb[2] = {0.0, 0.0};
@@ -623,13 +626,13 @@ __device__ __forceinline__ void phase_bisect_cands(const InstanceConsts& c, cons
   }
   int kl[2];
 #if HPS_BISECT_PROBES
-  b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
+  b = bisect_fast(c, tb, w, S, a, b, kb, kl);
 #else
-  const double bd = bisect_direct(c, w.st, w.row, S, a, b, kb, kl);
+  const double bd = bisect_direct(c, w, S, a, b, kb, kl);
   if (bd == bd) b = bd;
   else {  // (rare) seed too far off
     if (lane == 0) HPS_STAT(ST_UNPINNED, 1);
-    b = bisect_fast(c, tb, w.st, w.ent, S, a, b, kb, kl);
+    b = bisect_fast(c, tb, w, S, a, b, kb, kl);
   }
 #endif
   kb[0] = (double)kl[0];
@@ -641,9 +644,9 @@ __device__ __forceinline__ void phase_bisect_cands(const InstanceConsts& c, cons
 // Phase A: stages, optimize_k1 exits and the bisection. Returns false when the plan is
 // finished (infeasible / invalid); otherwise fills w.kmin/kmax and tau_lo/tau_hi.
 // Lane l holds digits d0 (layer l) and d1 (layer l+32).
-template <int MAXS, bool FAST = false, bool HI_ONLY = false>
+template <int MAXS, bool FAST = false, bool HI_ONLY = false, class W>
 __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables& tb,
-                                    WarpSmem<MAXS>& w, int d0, int d1, PlanOut& out,
+                                    W& w, int d0, int d1, PlanOut& out,
                                     double& tau_lo_out, double& tau_hi_out, int& n_cand) {
   const int lane = threadIdx.x & 31;
   const int L = c.L;
@@ -681,10 +684,10 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
     if (s < S) {
       const int type = (first < 32) ? t0 : t1;
       const int e = entry_index(c.P, type, first, last);
-      w.st[s] = tb.stages[e];
+      w.bind(s, tb.stages + e);
       w.ent[s] = e;
       w.row[s] = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
-      invalid |= (w.st[s].valid == 0);
+      invalid |= (w.stage(s).valid == 0);
     }
   }
   __syncwarp();
@@ -693,7 +696,7 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
     return false;
   }
   // --- stage-0 bound and tau_hi (ls/provisioner.py:394-397) ---
-  const int type0 = w.st[0].type;
+  const int type0 = w.stage(0).type;
   const int last0 = (S > 1) ? ((1 < c0) ? (int)__fns(m0, 0, 2) : 32 + (int)__fns(m1, 0, 1)) - 1 : L - 1;
   const Stage0Info s0 = tb.stage0[type0 * L + last0];
   if (s0.status != HPS_ST_OK) {
@@ -703,7 +706,7 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
   const double tau_hi = s0.tau_hi;
   // --- serial floor (ls/provisioner.py:399-412) ---
   double ser = 0.0;
-  for (int s = lane; s < S; s += 32) ser = fmax(ser, w.st[s].serial);
+  for (int s = lane; s < S; s += 32) ser = fmax(ser, w.stage(s).serial);
   ser = warp_max(ser);
   if (ser >= tau_hi) {
     out.status = HPS_ST_SERIAL; out.gap = clamp_gap((ser - tau_hi) / tau_hi);
@@ -719,9 +722,9 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
     const int s = lane + 32 * slot;
     if (s < S) {
       double r;
-      if (floor_count(w.st[s], tau_hi, c.bo, r, gapv[slot])) {
+      if (floor_count(w.stage(s), tau_hi, c.bo, r, gapv[slot])) {
         kb[slot] = iceil(r);
-        atomicAdd(&w.tsum[w.st[s].type], sat_count(kb[slot]));
+        atomicAdd(&w.tsum[w.stage(s).type], sat_count(kb[slot]));
       } else {
         raised[slot] = true;
       }
@@ -747,7 +750,7 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
       if (lane == 0) {
         u128 tot = 0;
         for (int s = 0; s < S; s++)
-          if (w.st[s].type == off) tot += dbl_to_u128(w.kres[s]);
+          if (w.stage(s).type == off) tot += dbl_to_u128(w.kres[s]);
         g = clamp_gap(int_true_div(tot - (u128)c.quota[off], c.quota[off]));
       }
       out.status = HPS_ST_QUOTA_TAU_HI; out.gap = __shfl_sync(0xffffffffu, g, 0);
@@ -781,8 +784,8 @@ __device__ bool phase_stages_bisect(const InstanceConsts& c, const DeviceTables&
       for (int slot = 0; slot < 2; slot++) {
         const int s = lane + 32 * slot;
         if (s < S) {
-          km[slot] = (ka[slot] == kb[slot]) ? kb[slot] : count_at(w.st[s], mid, c.bo);
-          if (km[slot] == inf) rz = true; else atomicAdd(&w.tsum[w.st[s].type], sat_count(km[slot]));
+          km[slot] = (ka[slot] == kb[slot]) ? kb[slot] : count_at(w.stage(s), mid, c.bo);
+          if (km[slot] == inf) rz = true; else atomicAdd(&w.tsum[w.stage(s).type], sat_count(km[slot]));
         }
       }
       __syncwarp();

@@ -1018,9 +1018,9 @@ stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src
              uint64_t p1, Outputs o, Pending pend, Cont cont, int feasible_only, KeyPart* parts,
              int first) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
+  WarpSmemL<MAXS>* sm = reinterpret_cast<WarpSmemL<MAXS>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpSmem<MAXS>& w = sm[warp];
+  WarpSmemL<MAXS>& w = sm[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   PlanState<MAXS>* states = reinterpret_cast<PlanState<MAXS>*>(cont.states);
   Key best;
@@ -1094,9 +1094,9 @@ template <int MAXS, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, HPS_STAGE_MINB / WARPS)
 bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending pend) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpSmem<MAXS>* sm = reinterpret_cast<WarpSmem<MAXS>*>(smem_raw);
+  WarpSmemL<MAXS>* sm = reinterpret_cast<WarpSmemL<MAXS>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpSmem<MAXS>& w = sm[warp];
+  WarpSmemL<MAXS>& w = sm[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   PlanState<MAXS>* states = reinterpret_cast<PlanState<MAXS>*>(cont.states);
   const unsigned int n = *cont.count;
@@ -1107,11 +1107,11 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
 #pragma unroll 1
     for (int s = lane; s < S; s += 32) {
       const int e = ps.ent[s];
-      const StageEntry st = tb.stages[e];
-      w.st[s] = st;
+      const int type = __ldg(&tb.stages[e].type);
+      w.sp[s] = tb.stages + e;
       w.ent[s] = e;
-      w.row[s] = tb.te + c.te_off[st.type] + (int64_t)(e - st.type * c.P) * (int64_t)(c.et_cap[st.type] + 1);
-      w.kmin[s] = (double)ps.kmin[s];
+      w.row[s] = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
+      w.kmin[s] = ps.kmin[s];
     }
     __syncwarp();
     double tau_lo;
@@ -1316,7 +1316,7 @@ template <int MAXS, int WARPS, bool ARGMIN, int SRC>
 int launch_stage(HpsInstance* in, const PlanSource& src, uint64_t p0, uint64_t p1, const Outputs& o,
                  Pending pend, Cont cont, int feasible_only, KeyPart* parts, int first, int grid,
                  cudaStream_t st) {
-  const size_t smem = sizeof(WarpSmem<MAXS>) * WARPS;
+  const size_t smem = sizeof(WarpSmemL<MAXS>) * WARPS;
   auto kern = stage_kernel<MAXS, WARPS, ARGMIN, SRC>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
@@ -1339,7 +1339,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
   const size_t smem2 = (sizeof(WarpSmemL<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
-  const size_t smem1 = sizeof(WarpSmem<MAXS>) * WARPS;
+  const size_t smem1 = sizeof(WarpSmemL<MAXS>) * WARPS;
   auto kb = bisect_kernel<MAXS, WARPS>;
   CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
   auto kp = prep_kernel<MAXS, WARPS>;
