@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "hps_sweep.cuh"
+#include "hps_tma.cuh"
 
 using namespace hps;
 
@@ -952,6 +953,7 @@ struct HpsInstance {
   int grid_per_sm = 16;   // blocks per SM of the split kernels' grid (HPS_GRID_PER_SM)
   int carveout = -1;      // shared-memory carveout % for the split kernels (HPS_CARVEOUT)
   size_t te_bytes = 0;    // threshold-table size (bounds of the checked build)
+  uint64_t chunk = 0;     // plans per split-kernel chunk (HPS_CHUNK; 0: by MAXS)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
 };
@@ -982,7 +984,7 @@ int chk_bind(const HpsInstance* in, cudaStream_t st) {
 // hot loop inside the instruction cache (one fused kernel stalled on instruction fetch).
 
 template <int MAXS>
-struct PlanState {
+struct __align__(16) PlanState {   // 16-byte multiple: staged by 1-D bulk copies
   uint64_t p, rank_hi, rank_lo;
   double tau_lo, tau_hi;
   int32_t S, n_cand;
@@ -996,6 +998,54 @@ struct Cont {
   unsigned int* count;
   unsigned int cap;   // PlanState slots (the chunk size)
 };
+
+// Per-plan result of cand_prep carried from prep_kernel to candidate_kernel.
+template <int MAXS>
+struct __align__(16) PrepState {
+  double ub;
+  int32_t top;
+  int8_t dom[MAXS], lead[MAXS];
+  int16_t alo[MAXS], an[MAXS], blo[MAXS];
+};
+
+// double-buffered per-warp staging of the next plan's state records (bulk copies, hps_tma.cuh)
+template <int MAXS, bool PREP>
+struct StageBuf {
+  PlanState<MAXS> ps[2];
+  PrepState<MAXS> pp[PREP ? 2 : 1];
+  uint64_t bar[2];
+};
+
+// shared-memory offset of the staging buffers: after the warp views and the sweep constants
+template <int MAXS, int WARPS>
+__host__ __device__ constexpr size_t stage_offset() {
+  return ((sizeof(WarpSmemL<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS + 15) / 16 * 16;
+}
+
+template <int MAXS, bool PREP>
+__device__ __forceinline__ void stage_init(StageBuf<MAXS, PREP>& sb) {
+  if ((threadIdx.x & 31) == 0) {
+    mbar_init(&sb.bar[0], 1);
+    mbar_init(&sb.bar[1], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+}
+
+// lane 0: stage plan q's PlanState (and PrepState) into slot `slot`; the slot's previous
+// contents were read by the whole warp before the __syncwarp that ended that iteration
+template <int MAXS, bool PREP>
+__device__ __forceinline__ void stage_issue(StageBuf<MAXS, PREP>& sb, int slot, const PlanState<MAXS>* states,
+                                            const PrepState<MAXS>* prep, uint64_t q) {
+  if ((threadIdx.x & 31) == 0) {
+    fence_proxy_async_smem();
+    const uint32_t bytes = sizeof(PlanState<MAXS>) + (PREP ? sizeof(PrepState<MAXS>) : 0);
+    mbar_arrive_expect_tx(&sb.bar[slot], bytes);
+    bulk_g2s(&sb.ps[slot], states + q, sizeof(PlanState<MAXS>), &sb.bar[slot]);
+    if (PREP) bulk_g2s(&sb.pp[slot & (PREP ? 1 : 0)], prep + q, sizeof(PrepState<MAXS>), &sb.bar[slot]);
+  }
+}
+
 
 __device__ __forceinline__ void merge_part(KeyPart* parts, uint64_t slot, int first, const Key& best,
                                            unsigned long long feas, uint32_t flags) {
@@ -1079,13 +1129,6 @@ stage_kernel(const InstanceConsts c, const DeviceTables tb, const PlanSource src
 #ifndef HPS_CAND_MINB
 #define HPS_CAND_MINB 32
 #endif
-// prefetch the next plan's state records into L2 (one 128-byte line per lane) while the
-// current plan is processed
-__device__ __forceinline__ void prefetch_lines(const void* base, size_t bytes) {
-  const int lane = threadIdx.x & 31;
-  if ((size_t)lane * 128 < bytes)
-    asm volatile("prefetch.global.L2 [%0];" :: "l"(reinterpret_cast<const char*>(base) + (size_t)lane * 128));
-}
 
 // K1a': the quota bisection (bisect_direct) and the candidate prefix of each surviving plan,
 // in place on its PlanState; plans with more than 4096 breakpoints go to the slow path and
@@ -1099,10 +1142,18 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
   WarpSmemL<MAXS>& w = sm[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   PlanState<MAXS>* states = reinterpret_cast<PlanState<MAXS>*>(cont.states);
+  StageBuf<MAXS, false>& sb = reinterpret_cast<StageBuf<MAXS, false>*>(
+      smem_raw + (sizeof(WarpSmemL<MAXS>) * WARPS + 15) / 16 * 16)[warp];
   const unsigned int n = *cont.count;
-  for (uint64_t q = gw; q < n; q += nw) {
-    if (q + nw < n) prefetch_lines(&states[q + nw], sizeof(PlanState<MAXS>));
-    PlanState<MAXS>& ps = states[q];
+  stage_init(sb);
+  if (gw < n) stage_issue(sb, 0, states, (const PrepState<MAXS>*)nullptr, gw);
+  uint32_t it = 0;
+  for (uint64_t q = gw; q < n; q += nw, it++) {
+    const int slot = it & 1;
+    if (q + nw < n) stage_issue(sb, slot ^ 1, states, (const PrepState<MAXS>*)nullptr, q + nw);
+    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
+    const PlanState<MAXS>& ps = sb.ps[slot];   // staged copy; results go to states[q]
+    PlanState<MAXS>& out = states[q];
     const int S = ps.S;
 #pragma unroll 1
     for (int s = lane; s < S; s += 32) {
@@ -1123,28 +1174,19 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
         const unsigned int at = atomicAdd(pend.count, 1u);
         HPS_CHECK(at < pend.cap, "pending list overflow");
         if (at < pend.cap) pend.list[at] = ps.p;
-        ps.n_cand = -1;
+        out.n_cand = -1;
       }
     } else {
-      for (int s = lane; s < S; s += 32) ps.kmax[s] = (int32_t)w.kmax[s];
-      for (int s = lane; s <= S; s += 32) ps.pre[s] = w.pre[s];
+      for (int s = lane; s < S; s += 32) out.kmax[s] = (int32_t)w.kmax[s];
+      for (int s = lane; s <= S; s += 32) out.pre[s] = w.pre[s];
       if (lane == 0) {
-        ps.tau_lo = tau_lo;
-        ps.n_cand = n_cand;
+        out.tau_lo = tau_lo;
+        out.n_cand = n_cand;
       }
     }
     __syncwarp();
   }
 }
-
-// Per-plan result of cand_prep carried from prep_kernel to candidate_kernel.
-template <int MAXS>
-struct PrepState {
-  double ub;
-  int32_t top;
-  int8_t dom[MAXS], lead[MAXS];
-  int16_t alo[MAXS], an[MAXS], blo[MAXS];
-};
 
 // load PlanState q into the warp's shared-memory view; per-stage constants of the sweep
 template <int MAXS>
@@ -1179,11 +1221,17 @@ prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<
   SweepSmem<MAXS>& sw = ss[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
+  StageBuf<MAXS, false>& sb = reinterpret_cast<StageBuf<MAXS, false>*>(smem_raw + stage_offset<MAXS, WARPS>())[warp];
   const unsigned int n = *cont.count;
-  for (uint64_t q = gw; q < n; q += nw) {
-    if (q + nw < n) prefetch_lines(&states[q + nw], sizeof(PlanState<MAXS>));
-    const PlanState<MAXS>& ps = states[q];
-    if (ps.n_cand < 0) continue;  // slow path
+  stage_init(sb);
+  if (gw < n) stage_issue(sb, 0, states, (const PrepState<MAXS>*)nullptr, gw);
+  uint32_t it = 0;
+  for (uint64_t q = gw; q < n; q += nw, it++) {
+    const int slot = it & 1;
+    if (q + nw < n) stage_issue(sb, slot ^ 1, states, (const PrepState<MAXS>*)nullptr, q + nw);
+    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
+    const PlanState<MAXS>& ps = sb.ps[slot];
+    if (ps.n_cand < 0) { __syncwarp(); continue; }  // slow path
     load_state<MAXS>(c, tb, ps, w);
     const int S = ps.S;
     TieBuf buf;
@@ -1218,6 +1266,8 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
   SweepSmem<MAXS>& sw = ss[warp];
   const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
   const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
+  StageBuf<MAXS, true>& sb = reinterpret_cast<StageBuf<MAXS, true>*>(
+      smem_raw + stage_offset<MAXS, WARPS>())[warp];
   const unsigned int n = *cont.count;
   Key best;
   best.cost = __longlong_as_double(0x7ff0000000000000LL);
@@ -1225,13 +1275,18 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
   best.status = 0;
   unsigned long long feas = 0;
   uint32_t flags = 0;
-  for (uint64_t q = gw; q < n; q += nw) {
-    if (q + nw < n) { prefetch_lines(&states[q + nw], sizeof(PlanState<MAXS>)); prefetch_lines(&prep[q + nw], sizeof(PrepState<MAXS>)); }
-    const PlanState<MAXS>& ps = states[q];
-    if (ps.n_cand < 0) continue;  // slow path
+  stage_init(sb);
+  if (gw < n) stage_issue(sb, 0, states, prep, gw);
+  uint32_t it = 0;
+  for (uint64_t q = gw; q < n; q += nw, it++) {
+    const int slot = it & 1;
+    if (q + nw < n) stage_issue(sb, slot ^ 1, states, prep, q + nw);
+    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
+    const PlanState<MAXS>& ps = sb.ps[slot];
+    if (ps.n_cand < 0) { __syncwarp(); continue; }  // slow path
     load_state<MAXS>(c, tb, ps, w);
     const int S = ps.S;
-    const PrepState<MAXS>& pp = prep[q];
+    const PrepState<MAXS>& pp = sb.pp[slot];
 #pragma unroll 1
     for (int r = lane; r < S; r += 32) {
       const int lo = ps.kmin[r], hi = ps.kmax[r];
@@ -1330,7 +1385,8 @@ int launch_stage(HpsInstance* in, const PlanSource& src, uint64_t p0, uint64_t p
 template <int MAXS, int WARPS, bool ARGMIN>
 int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
               int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
-  const uint64_t chunk = std::min<uint64_t>(n, MAXS <= 16 ? (4ull << 20) : (MAXS <= 32 ? (2ull << 20) : (1ull << 20)));
+  const uint64_t base_chunk = in->chunk ? in->chunk : (MAXS <= 16 ? (4ull << 20) : (MAXS <= 32 ? (2ull << 20) : (1ull << 20)));
+  const uint64_t chunk = std::min<uint64_t>(n, base_chunk);
   char* buf = nullptr;
   const size_t state_bytes = (sizeof(PlanState<MAXS>) * chunk + 255) / 256 * 256;
   CUDA_TRY(cudaMallocAsync(&buf, state_bytes + sizeof(PrepState<MAXS>) * chunk + 256, st));
@@ -1338,14 +1394,15 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(buf + 256 + state_bytes);
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
-  const size_t smem2 = (sizeof(WarpSmemL<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS;
-  const size_t smem1 = sizeof(WarpSmemL<MAXS>) * WARPS;
+  const size_t smem3 = stage_offset<MAXS, WARPS>() + sizeof(StageBuf<MAXS, true>) * WARPS;   // + staging
+  const size_t smem1 = (sizeof(WarpSmemL<MAXS>) * WARPS + 15) / 16 * 16 + sizeof(StageBuf<MAXS, false>) * WARPS;
   auto kb = bisect_kernel<MAXS, WARPS>;
   CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
   auto kp = prep_kernel<MAXS, WARPS>;
-  CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  const size_t smemp = stage_offset<MAXS, WARPS>() + sizeof(StageBuf<MAXS, false>) * WARPS;
+  CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemp));
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
-  CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
   for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
     const uint64_t c1 = std::min(n, c0 + chunk);
@@ -1361,10 +1418,10 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     kb<<<grid, WARPS * 32, smem1, st>>>(in->c, in->tb, cont, pend);
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
-    kp<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, prep);
+    kp<<<grid, WARPS * 32, smemp, st>>>(in->c, in->tb, cont, prep);
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
-    k2<<<grid, WARPS * 32, smem2, st>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
+    k2<<<grid, WARPS * 32, smem3, st>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaFreeAsync(buf, st));
@@ -1562,6 +1619,7 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   cudaDeviceGetAttribute(&in->sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (const char* e = getenv("HPS_GRID_PER_SM")) in->grid_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("HPS_CARVEOUT")) in->carveout = std::min(100, atoi(e));
+  if (const char* e = getenv("HPS_CHUNK")) in->chunk = (uint64_t)std::max(1024ll, atoll(e));
   if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls
     cudaMemPool_t pool;
