@@ -954,6 +954,7 @@ struct HpsInstance {
   int carveout = -1;      // shared-memory carveout % for the split kernels (HPS_CARVEOUT)
   size_t te_bytes = 0;    // threshold-table size (bounds of the checked build)
   uint64_t chunk = 0;     // plans per split-kernel chunk (HPS_CHUNK; 0: by MAXS)
+  bool half_bisect = true;  // L <= 16: two plans per warp in the bisection (HPS_HALF_BISECT=0: one)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
 };
@@ -1188,6 +1189,10 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
   }
 }
 
+}  // namespace
+#include "hps_half.cuh"
+namespace {
+
 // load PlanState q into the warp's shared-memory view; per-stage constants of the sweep
 template <int MAXS>
 __device__ __forceinline__ void load_state(const InstanceConsts& c, const DeviceTables& tb, const PlanState<MAXS>& ps,
@@ -1398,6 +1403,9 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   const size_t smem1 = (sizeof(WarpSmemL<MAXS>) * WARPS + 15) / 16 * 16 + sizeof(StageBuf<MAXS, false>) * WARPS;
   auto kb = bisect_kernel<MAXS, WARPS>;
   CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  auto kbh = bisect_kernel_h<WARPS>;
+  const size_t smemh = (sizeof(WarpSmemL<16>) * WARPS * 2 + 15) / 16 * 16 + sizeof(StageBuf<16, false>) * WARPS * 2;
+  if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(kbh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemh));
   auto kp = prep_kernel<MAXS, WARPS>;
   const size_t smemp = stage_offset<MAXS, WARPS>() + sizeof(StageBuf<MAXS, false>) * WARPS;
   CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemp));
@@ -1415,7 +1423,11 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
     if (rc) return rc;
     HPS_COUNT_LAUNCH();
-    kb<<<grid, WARPS * 32, smem1, st>>>(in->c, in->tb, cont, pend);
+    if (MAXS == 16 && in->half_bisect) {   // two plans per warp (hps_half.cuh)
+      kbh<<<grid, WARPS * 32, smemh, st>>>(in->c, in->tb, cont, pend);
+    } else {
+      kb<<<grid, WARPS * 32, smem1, st>>>(in->c, in->tb, cont, pend);
+    }
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
     kp<<<grid, WARPS * 32, smemp, st>>>(in->c, in->tb, cont, prep);
@@ -1619,6 +1631,7 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   cudaDeviceGetAttribute(&in->sm_count, cudaDevAttrMultiProcessorCount, dev);
   if (const char* e = getenv("HPS_GRID_PER_SM")) in->grid_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("HPS_CARVEOUT")) in->carveout = std::min(100, atoi(e));
+  if (const char* e = getenv("HPS_HALF_BISECT")) in->half_bisect = atoi(e) != 0;
   if (const char* e = getenv("HPS_CHUNK")) in->chunk = (uint64_t)std::max(1024ll, atoll(e));
   if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls
