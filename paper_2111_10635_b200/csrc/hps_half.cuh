@@ -4,46 +4,50 @@
 // idle, and the warp-uniform parts (the per-type threshold search and the reference's 60
 // replayed halvings) run once per plan. Here each 16-lane half of a warp owns one plan: every
 // warp-wide step becomes a 16-lane segment step (xor / up shuffles by 8, 4, 2, 1 stay inside a
-// half; masks come from __activemask, so the halves may take different paths), and whatever
+// half; each collective names its own half, so the halves may take different paths), and whatever
 // the two plans do alike issues once for both. Same arithmetic as bisect_direct /
 // cands_prefix (hps_eval.cuh), so the same bits.
 #pragma once
 
 namespace hps {
 
+// the 16 lanes of this thread's half: every collective below names exactly its segment (the two
+// halves may be at different points of their plans; each half's lanes all reach each call)
+__device__ __forceinline__ unsigned seg_mask() { return 0xffffu << (threadIdx.x & 16); }
+
 __device__ __forceinline__ double seg_max(double v) {
-  const unsigned am = __activemask();
+  const unsigned am = seg_mask();
 #pragma unroll
   for (int o = 8; o; o >>= 1) { const double u = __shfl_xor_sync(am, v, o); v = (u > v) ? u : v; }
   return v;
 }
 __device__ __forceinline__ double seg_min(double v) {
-  const unsigned am = __activemask();
+  const unsigned am = seg_mask();
 #pragma unroll
   for (int o = 8; o; o >>= 1) { const double u = __shfl_xor_sync(am, v, o); v = (u < v) ? u : v; }
   return v;
 }
 __device__ __forceinline__ int seg_sum(int v) {
-  const unsigned am = __activemask();
+  const unsigned am = seg_mask();
 #pragma unroll
   for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(am, v, o);
   return v;
 }
 __device__ __forceinline__ float seg_sumf(float v) {
-  const unsigned am = __activemask();
+  const unsigned am = seg_mask();
 #pragma unroll
   for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(am, v, o);
   return v;
 }
 __device__ __forceinline__ unsigned seg_or(unsigned v) {
-  const unsigned am = __activemask();
+  const unsigned am = seg_mask();
 #pragma unroll
   for (int o = 8; o; o >>= 1) v |= __shfl_xor_sync(am, v, o);
   return v;
 }
 // this half's 16 ballot bits (bit i = segment lane i)
 __device__ __forceinline__ unsigned seg_ballot(bool p) {
-  const unsigned m = __ballot_sync(__activemask(), p);
+  const unsigned m = __ballot_sync(seg_mask(), p);
   return (m >> (threadIdx.x & 16)) & 0xffffu;
 }
 
@@ -148,7 +152,7 @@ __device__ void cands_prefix_half(const DeviceTables& tb, W& w, int S, int kb, i
     w.kmax[sl] = kb;
     w.cls[sl] = tb_class(tb, w.ent[sl]);
   }
-  __syncwarp(__activemask());
+  __syncwarp(seg_mask());
   int cnt = 0;
   if (sl < S) {
     bool leader = true;
@@ -157,7 +161,7 @@ __device__ void cands_prefix_half(const DeviceTables& tb, W& w, int S, int kb, i
     const int span = w.kmax[sl] - w.kmin[sl];
     if (leader && span <= kBpLimit) cnt = span + 1;
   }
-  const unsigned am = __activemask();
+  const unsigned am = seg_mask();
   int inc = cnt;
 #pragma unroll
   for (int o = 1; o < 16; o <<= 1) {
@@ -214,7 +218,7 @@ bisect_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, Pendin
       w.row[sl] = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
       w.kmin[sl] = ps.kmin[sl];
     }
-    __syncwarp(__activemask());
+    __syncwarp(seg_mask());
     int klo = 0;
     const double tau_lo = bisect_half(c, w, S, ps.tau_lo, ps.tau_hi, (sl < S) ? ps.kmin[sl] : 0, klo);
     int n_cand = kBpLimit + 1;   // NaN tau_lo (poor seed): the slow path finishes the plan
@@ -238,8 +242,125 @@ bisect_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, Pendin
         out.n_cand = n_cand;
       }
     }
-    __syncwarp(__activemask());
+    __syncwarp(seg_mask());
   }
+}
+
+}  // namespace hps
+
+namespace hps {
+
+__device__ __forceinline__ unsigned long long seg_sum_u64(unsigned long long v) {
+  const unsigned am = seg_mask();
+#pragma unroll
+  for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(am, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long seg_or_u64(unsigned long long v) {
+  const unsigned am = seg_mask();
+#pragma unroll
+  for (int o = 8; o; o >>= 1) v |= __shfl_xor_sync(am, v, o);
+  return v;
+}
+
+// phase_stages_bisect<16, true, true> (hps_eval.cuh) for the plan of this half: runs, stages,
+// min_k1 / tau_hi, serial floor, counts at tau_hi and the quota check (ls/provisioner.py:
+// 394-427). Segment lane sl holds the digit of layer sl and builds stage sl.
+template <class W>
+__device__ bool stage_phase_half(const InstanceConsts& c, const DeviceTables& tb, W& w, int d, PlanOut& out,
+                                 double& tau_lo_out, double& tau_hi_out) {
+  const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
+  const int L = c.L;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const unsigned am = seg_mask();
+  const int prev = __shfl_up_sync(am, d, 1);   // (segment lane 0 ignores it)
+  const bool start = (sl < L) && (sl == 0 || d != prev);
+  const unsigned m = seg_ballot(start);
+  if (seg_ballot(sl < L && (d < 0 || d >= c.T))) {
+    out.status = HPS_ST_INVALID; out.cost = __longlong_as_double(0x7ff8000000000000LL); out.gap = 0; out.S = 0;
+    return false;
+  }
+  const int S = __popc(m);
+  out.S = S;
+  int first = 0, last = 0;
+  if (sl < S) {
+    first = (int)__fns(m, 0, sl + 1);
+    last = (sl + 1 < S) ? (int)__fns(m, 0, sl + 2) - 1 : L - 1;
+  }
+  const int type = __shfl_sync(am, d, base + (first & 15));
+  bool invalid = false;
+  if (sl < S) {
+    const int e = entry_index(c.P, type, first, last);
+    w.bind(sl, tb.stages + e);
+    w.ent[sl] = e;
+    w.row[sl] = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
+    invalid = (w.stage(sl).valid == 0);
+  }
+  __syncwarp(am);
+  if (seg_ballot(invalid)) {
+    out.status = HPS_ST_INVALID; out.cost = __longlong_as_double(0x7ff8000000000000LL); out.gap = 0;
+    return false;
+  }
+  // stage-0 bound and tau_hi (ls/provisioner.py:394-397)
+  const int type0 = w.stage(0).type;
+  const int last0 = (S > 1) ? (int)__fns(m, 0, 2) - 1 : L - 1;
+  const Stage0Info s0 = tb.stage0[type0 * L + last0];
+  if (s0.status != HPS_ST_OK) {
+    out.status = s0.status; out.gap = s0.gap; out.cost = c.penalty_scale * (1.0 + pmax(0.0, s0.gap));
+    return false;
+  }
+  const double tau_hi = s0.tau_hi;
+  // serial floor (ls/provisioner.py:399-412)
+  const double ser = seg_max((sl < S) ? fmax(0.0, w.stage(sl).serial) : 0.0);
+  if (ser >= tau_hi) {
+    out.status = HPS_ST_SERIAL; out.gap = clamp_gap((ser - tau_hi) / tau_hi);
+    out.cost = c.penalty_scale * (1.0 + pmax(0.0, out.gap));
+    return false;
+  }
+  // counts at tau_hi and the quotas (ls/provisioner.py:413-427)
+  double kb = inf, gapv = 0.0;
+  bool raised = false;
+  const int ty = (sl < S) ? w.stage(sl).type : -1;
+  if (sl < S) {
+    double r;
+    if (floor_count(w.stage(sl), tau_hi, c.bo, r, gapv)) kb = iceil(r); else raised = true;
+  }
+  const unsigned rm = seg_ballot(raised);
+  unsigned over = 0;
+  if (!rm) {
+    unsigned present = seg_or(ty >= 0 ? 1u << ty : 0u);
+    while (present) {
+      const int t = __ffs(present) - 1;
+      present &= present - 1;
+      const unsigned long long sum = seg_sum_u64(ty == t ? sat_count(kb) : 0ull);
+      if (sum > (unsigned long long)c.quota[t]) over |= 1u << t;
+    }
+  }
+  if (rm | over) {
+    if (rm) {   // _counts_at(tau_hi) raises from the first raising stage (:414)
+      out.status = HPS_ST_FLOOR_TAU_HI;
+      out.gap = __shfl_sync(am, gapv, base + __ffs(rm) - 1);
+    } else {    // first offending type in ascending id (:418-420), exact Python-int totals
+      if (sl < S) w.kres[sl] = kb;
+      __syncwarp(am);
+      const int off = __ffs(over) - 1;
+      double g = 0.0;
+      if (sl == 0) {
+        u128 tot = 0;
+        for (int s = 0; s < S; s++)
+          if (w.stage(s).type == off) tot += dbl_to_u128(w.kres[s]);
+        g = clamp_gap(int_true_div(tot - (u128)c.quota[off], c.quota[off]));
+      }
+      out.status = HPS_ST_QUOTA_TAU_HI;
+      out.gap = __shfl_sync(am, g, base);
+    }
+    out.cost = c.penalty_scale * (1.0 + pmax(0.0, out.gap));
+    return false;
+  }
+  if (sl < S) w.kmin[sl] = (int)kb;
+  tau_hi_out = tau_hi;
+  tau_lo_out = ser;
+  return true;
 }
 
 }  // namespace hps

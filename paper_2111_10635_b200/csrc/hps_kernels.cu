@@ -955,6 +955,7 @@ struct HpsInstance {
   size_t te_bytes = 0;    // threshold-table size (bounds of the checked build)
   uint64_t chunk = 0;     // plans per split-kernel chunk (HPS_CHUNK; 0: by MAXS)
   bool half_bisect = true;  // L <= 16: two plans per warp in the bisection (HPS_HALF_BISECT=0: one)
+  bool half_stage = true;   // L <= 16: two plans per warp in the stage kernel (HPS_HALF_STAGE=0: one)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
 };
@@ -1193,6 +1194,141 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
 #include "hps_half.cuh"
 namespace {
 
+// load_digits for a plan per 16-lane half: segment lane sl gets the digit of layer sl (L <= 16)
+template <int MODE>
+__device__ __forceinline__ void load_digits_half(const InstanceConsts& c, const PlanSource& src, uint64_t p,
+                                                 int& d, u128& rank) {
+  const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
+  const int L = c.L;
+  d = 0;
+  rank = 0;
+  if (MODE == 1 || MODE == 3) {
+    uint64_t idx;
+    if (MODE == 1) {
+      idx = src.begin + p * src.stride;
+    } else {
+      const uint64_t q = src.begin + p;
+      const uint64_t r = q / src.stride;
+      idx = (uint64_t)__ldg(src.prefixes + r) * src.stride + (q - r * src.stride);
+    }
+    if (sl < L) {
+      if (idx < 0xffffffffull && src.tpow[0] < 0xffffffffull)
+        d = (int)(((uint32_t)idx / (uint32_t)src.tpow[sl]) % (uint32_t)c.T);
+      else
+        d = (int)((idx / src.tpow[sl]) % (uint64_t)c.T);
+    }
+    rank = idx;
+    return;
+  }
+  if (MODE == 0) {
+    if (sl < L) d = src.plans[p * (uint64_t)L + sl];
+  } else {   // numpy PCG64 integers(): 32-bit half h = g*L + l of the stream, low half first
+    const uint64_t g = src.begin + p;
+    if (c.T > 1) {
+      const u128 h0 = (u128)g * (u128)L;
+      const u128 hb = h0 >> 1;
+      u128 sb = 0;
+      if (sl == 0) sb = pcg_advance(mk(src.s0_hi, src.s0_lo), mk(src.inc_hi, src.inc_lo), hb + 1);
+      const unsigned am = seg_mask();
+      sb = mk(__shfl_sync(am, (uint64_t)(sb >> 64), base), __shfl_sync(am, (uint64_t)sb, base));
+      if (sl < L) {
+        const u128 h = h0 + (u128)sl;
+        const int j = (int)((h >> 1) - hb);
+        const u128 st = mk(src.jA_hi[j], src.jA_lo[j]) * sb + mk(src.jC_hi[j], src.jC_lo[j]);
+        const uint64_t v = pcg_output(st);
+        const uint32_t u = (h & 1) ? (uint32_t)(v >> 32) : (uint32_t)v;
+        d = (int)(u >> (32 - src.tbits));
+      }
+    }
+  }
+  if (MODE == 2 || src.tbits > 0) {   // packed lexicographic rank, layer 0 most significant
+    u128 part = 0;
+    if (sl < L) part = (u128)(d & ((1 << src.tbits) - 1)) << ((L - 1 - sl) * src.tbits);
+    rank = mk(seg_or_u64((uint64_t)(part >> 64)), seg_or_u64((uint64_t)part));
+  }
+}
+
+// stage_kernel with two plans per warp (L <= 16, hps_half.cuh)
+template <int WARPS, bool ARGMIN, int SRC>
+__global__ void __launch_bounds__(WARPS * 32, HPS_STAGE_MINB / WARPS)
+stage_kernel_h(const InstanceConsts c, const DeviceTables tb, const PlanSource src, uint64_t p0,
+               uint64_t p1, Outputs o, Pending pend, Cont cont, int feasible_only, KeyPart* parts,
+               int first) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, sl = lane & 15;
+  WarpSmemL<16>& w = reinterpret_cast<WarpSmemL<16>*>(smem_raw)[warp * 2 + half];
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp, nw = (uint64_t)gridDim.x * WARPS;
+  const uint64_t gh = gw * 2 + half, nh = nw * 2;
+  PlanState<16>* states = reinterpret_cast<PlanState<16>*>(cont.states);
+  Key best;
+  best.cost = __longlong_as_double(0x7ff0000000000000LL);
+  best.hi = best.lo = ~0ull;
+  best.status = 0;
+  uint32_t flags = 0;
+  for (uint64_t p = p0 + gh; p < p1; p += nh) {
+    int d;
+    u128 rank;
+    load_digits_half<SRC>(c, src, p, d, rank);
+    PlanOut r;
+    r.ps = 0;
+    r.gap = 0.0;
+    double tau_lo, tau_hi;
+    if (stage_phase_half(c, tb, w, d, r, tau_lo, tau_hi)) {
+      const unsigned am = seg_mask();
+      unsigned int at = 0;
+      if (sl == 0) at = atomicAdd(cont.count, 1u);
+      at = __shfl_sync(am, at, lane & 16);
+      HPS_CHECK(at < cont.cap, "plan-state chunk overflow");
+      PlanState<16>& ps = states[at];
+      if (sl < r.S) {
+        ps.ent[sl] = w.ent[sl];
+        ps.kmin[sl] = w.kmin[sl];
+      }
+      if (sl == 0) {
+        ps.p = p;
+        ps.rank_hi = (uint64_t)(rank >> 64);
+        ps.rank_lo = (uint64_t)rank;
+        ps.tau_lo = tau_lo;
+        ps.tau_hi = tau_hi;
+        ps.S = r.S;
+        ps.n_cand = 0;
+      }
+    } else if (!ARGMIN) {   // write_plan for this half's plan
+      const bool ok = (r.status & 0x7f) == HPS_ST_OK;
+      if (sl == 0) {
+        o.cost[p] = r.cost;
+        o.status[p] = (uint8_t)r.status;
+        if (o.gap) o.gap[p] = r.gap;
+        if (o.ps) o.ps[p] = ok ? r.ps : 0;
+        if (o.num_stages) o.num_stages[p] = r.S;
+      }
+      if (o.k)
+        for (int s = sl; s < c.L; s += 16) o.k[p * (uint64_t)c.L + s] = 0;   // infeasible here
+    } else {
+      const int code = r.status & 0x7f;
+      if (code == HPS_ST_NO_CPU_TYPE) flags |= 1u;
+      if (code == HPS_ST_INVALID) flags |= 2u;
+      const bool take = feasible_only ? false : (code != HPS_ST_NO_CPU_TYPE && code != HPS_ST_INVALID);
+      if (take) {
+        Key k{r.cost, (uint64_t)(rank >> 64), (uint64_t)rank, (uint32_t)r.status};
+        if (key_less(k, best)) best = k;
+      }
+    }
+    __syncwarp(seg_mask());
+  }
+  if (ARGMIN) {   // the two halves' partials meet, lane 0 writes the warp's
+    __syncwarp();
+    Key ob;
+    ob.cost = __shfl_xor_sync(0xffffffffu, best.cost, 16);
+    ob.hi = __shfl_xor_sync(0xffffffffu, best.hi, 16);
+    ob.lo = __shfl_xor_sync(0xffffffffu, best.lo, 16);
+    ob.status = __shfl_xor_sync(0xffffffffu, best.status, 16);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 16);
+    if (key_less(ob, best)) best = ob;
+    if (lane == 0) merge_part(parts, gw, first, best, 0ull, flags);
+  }
+}
+
 // load PlanState q into the warp's shared-memory view; per-stage constants of the sweep
 template <int MAXS>
 __device__ __forceinline__ void load_state(const InstanceConsts& c, const DeviceTables& tb, const PlanState<MAXS>& ps,
@@ -1376,6 +1512,15 @@ template <int MAXS, int WARPS, bool ARGMIN, int SRC>
 int launch_stage(HpsInstance* in, const PlanSource& src, uint64_t p0, uint64_t p1, const Outputs& o,
                  Pending pend, Cont cont, int feasible_only, KeyPart* parts, int first, int grid,
                  cudaStream_t st) {
+  if (MAXS == 16 && in->half_stage) {   // two plans per warp (hps_half.cuh)
+    const size_t smem = sizeof(WarpSmemL<16>) * WARPS * 2;
+    auto kern = stage_kernel_h<WARPS, ARGMIN, SRC>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HPS_COUNT_LAUNCH();
+    kern<<<grid, WARPS * 32, smem, st>>>(in->c, in->tb, src, p0, p1, o, pend, cont, feasible_only, parts, first);
+    CUDA_TRY(cudaGetLastError());
+    return HPS_OK;
+  }
   const size_t smem = sizeof(WarpSmemL<MAXS>) * WARPS;
   auto kern = stage_kernel<MAXS, WARPS, ARGMIN, SRC>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1632,6 +1777,7 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   if (const char* e = getenv("HPS_GRID_PER_SM")) in->grid_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("HPS_CARVEOUT")) in->carveout = std::min(100, atoi(e));
   if (const char* e = getenv("HPS_HALF_BISECT")) in->half_bisect = atoi(e) != 0;
+  if (const char* e = getenv("HPS_HALF_STAGE")) in->half_stage = atoi(e) != 0;
   if (const char* e = getenv("HPS_CHUNK")) in->chunk = (uint64_t)std::max(1024ll, atoll(e));
   if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls
