@@ -1409,6 +1409,9 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
   const PlanState<MAXS>* states = reinterpret_cast<const PlanState<MAXS>*>(cont.states);
   StageBuf<MAXS, true>& sb = reinterpret_cast<StageBuf<MAXS, true>*>(
       smem_raw + stage_offset<MAXS, WARPS>())[warp];
+  CandQueue* queues = reinterpret_cast<CandQueue*>(smem_raw + stage_offset<MAXS, WARPS>() +
+                                                   sizeof(StageBuf<MAXS, true>) * WARPS);
+  if (lane == 0) sw.cq = &queues[warp];
   const unsigned int n = *cont.count;
   Key best;
   best.cost = __longlong_as_double(0x7ff0000000000000LL);
@@ -1544,7 +1547,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(buf + 256 + state_bytes);
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
-  const size_t smem3 = stage_offset<MAXS, WARPS>() + sizeof(StageBuf<MAXS, true>) * WARPS;   // + staging
+  const size_t smem3 = stage_offset<MAXS, WARPS>() + (sizeof(StageBuf<MAXS, true>) + sizeof(CandQueue)) * WARPS;
   const size_t smem1 = (sizeof(WarpSmemL<MAXS>) * WARPS + 15) / 16 * 16 + sizeof(StageBuf<MAXS, false>) * WARPS;
   auto kb = bisect_kernel<MAXS, WARPS>;
   CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));

@@ -29,6 +29,11 @@ namespace hps {
 #endif
 constexpr int kTop = HPS_TOP;   // unpinned stages bounded per candidate (count_lb32)
 
+struct CandQueue {    // survivors of cand_main's lower-bound filter, evaluated 32 at a time
+  double q[64];
+  int32_t qg[64];      // their generator: (leader << 16) | m, or -1 (tau_lo / tau_hi)
+};
+
 template <int MAXS>
 struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase (broadcast reads)
   double pr[MAXS];   // price per second of stage r's type
@@ -44,8 +49,7 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   float est[MAXS][6];  // count_est seed constants (est_setup)
   int8_t lead[MAXS]; // class leader of stage r (stages of one class have identical counts)
   int32_t gex[MAXS]; // leader r: count_r(et_r(m)) == m for m <= gex[r] (tb.gex), else 0
-  double q[64];      // survivors of the lower-bound filter, evaluated 32 at a time
-  int32_t qg[64];    // their generator: (leader << 16) | m, or -1 (tau_lo / tau_hi)
+  struct CandQueue* cq;  // the candidate kernel's survivor queue (prep does not need one)
   double p0;         // sum over pinned stages of pr * count (the bound's linear part)
   int32_t nu;        // unpinned stages, in stage order:
   int8_t ulist[MAXS];
@@ -558,12 +562,12 @@ __device__ double cand_main(const InstanceConsts& c, const W& w, SweepSmem<MAXS>
       }
     }
     const unsigned mk = __ballot_sync(0xffffffffu, keep);
-    if (keep) { sw.q[qn + __popc(mk & lt)] = tau; sw.qg[qn + __popc(mk & lt)] = gen; }
+    if (keep) { sw.cq->q[qn + __popc(mk & lt)] = tau; sw.cq->qg[qn + __popc(mk & lt)] = gen; }
     qn += __popc(mk);
     __syncwarp();
     if (qn >= 32) {
-      const double t = sw.q[qn - 32 + lane];
-      const int tg = sw.qg[qn - 32 + lane];
+      const double t = sw.cq->q[qn - 32 + lane];
+      const int tg = sw.cq->qg[qn - 32 + lane];
       HPS_STAT(ST_CANDS, 1);
       eval_insert<MAXS>(cs, w, sw, S, t, tg, buf);
       qn -= 32;
@@ -573,9 +577,9 @@ __device__ double cand_main(const InstanceConsts& c, const W& w, SweepSmem<MAXS>
   }
   if (qn > 0) {
     if (lane < qn) {
-      const double t = sw.q[lane];
+      const double t = sw.cq->q[lane];
       HPS_STAT(ST_CANDS, 1);
-      eval_insert<MAXS>(cs, w, sw, S, t, sw.qg[lane], buf);
+      eval_insert<MAXS>(cs, w, sw, S, t, sw.cq->qg[lane], buf);
     }
   }
   const double mf = warp_min(buf.mn);
@@ -596,6 +600,9 @@ __device__ double phase_candidates_fast(const InstanceConsts& c, const DeviceTab
                                         double tau_lo, double tau_hi, int n_cand) {
   TieBuf buf;
   buf.init();
+  __shared__ CandQueue fused_queue[32];   // (fused eval_kernel path only; <= 32 warps per block)
+  if ((threadIdx.x & 31) == 0) sw.cq = &fused_queue[threadIdx.x >> 5];
+  __syncwarp();
   const double ub = cand_prep<MAXS>(c, tb, w, sw, S, tau_lo, tau_hi, n_cand, buf);
   return cand_main<MAXS>(c, w, sw, S, tau_lo, tau_hi, ub, buf);
 }
