@@ -364,3 +364,172 @@ __device__ bool stage_phase_half(const InstanceConsts& c, const DeviceTables& tb
 }
 
 }  // namespace hps
+
+namespace hps {
+
+__device__ __forceinline__ double seg_sumd(double v) {
+  const unsigned am = seg_mask();
+#pragma unroll
+  for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(am, v, o);
+  return v;
+}
+
+// interval_cells (hps_sweep.cuh) for the plan of this half: segment lane j holds grid point j
+__device__ __noinline__ void interval_cells_half(double t, double L, double d, double thr, double& ta, double& tb) {
+  const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
+  const unsigned am = seg_mask();
+  const double t1 = __shfl_down_sync(am, t, 1, 16);
+  const double L1 = __shfl_down_sync(am, L, 1, 16);
+  const double d1 = __shfl_down_sync(am, d, 1, 16);
+  double lb;
+  if (d >= 0.0) lb = L;
+  else if (d1 <= 0.0) lb = L1;
+  else {
+    const double x = (L1 - L + d * t - d1 * t1) * rcp_1nt(d - d1);
+    lb = fmin(fmin(L + d * (x - t), L1 + d1 * (x - t1)), fmin(L, L1));
+  }
+  const bool keep = (sl < kGrid - 1) && !(lb > thr);   // NaN keeps
+  const unsigned mk = seg_ballot(keep);
+  if (!mk) { ta = 1.0; tb = 0.0; return; }
+  const int f = __ffs(mk) - 1, l = 31 - __clz(mk);
+  const double nta = __shfl_sync(am, t, base + f);
+  tb = __shfl_sync(am, t, base + l + 1);
+  ta = nta;
+}
+
+// cand_prep (hps_sweep.cuh) for the plan of this half (S <= 16): segment lane sl owns stage sl
+// and grid point sl; the warm start evaluates the same 32 candidates in two rounds of 16.
+template <int MAXS, class W>
+__device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb, const W& w, SweepSmem<MAXS>& sw,
+                                 int S, double tau_lo, double tau_hi, int n_cand, TieBuf& buf) {
+  const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
+  const unsigned am = seg_mask();
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const int r = sl;
+  const bool mine = r < S;
+  const bool pinned = mine && (w.kmax[r] == w.kmin[r]);
+  if (mine) {
+    sw.pr[r] = c.price_s[w.stage(r).type];
+    sw.fpr[r] = (float)sw.pr[r];
+    sw.kmi[r] = (int)w.kmin[r];
+    sw.kma[r] = (int)w.kmax[r];
+    sw.etp[r] = pinned ? HPS_TE(w.row[r], (int)w.kmin[r] - 1).et : 0.0;
+    sw.dom[r] = pinned ? 0 : side_dominance(w.stage(r), tau_lo, tau_hi, c.bo);
+    est_setup<MAXS>(w, sw, r);
+    int ld = 0;
+    while (w.cls[ld] != w.cls[r]) ld++;
+    sw.lead[r] = (int8_t)ld;
+    sw.gex[r] = (ld == r && !pinned) ? __ldg(tb.gex + w.ent[r]) : 0;
+  }
+  {  // unpinned stages in order, and the pinned stages' part of the bound
+    const bool unp = mine && !pinned;
+    const double p0 = seg_sumd((mine && pinned) ? c.price_s[w.stage(r).type] * w.kmin[r] : 0.0);
+    const unsigned m = seg_ballot(unp);
+    if (unp) sw.ulist[__popc(m & ((1u << sl) - 1u))] = (int8_t)r;
+    if (sl == 0) { sw.nu = __popc(m); sw.p0 = p0; }
+  }
+  __syncwarp(am);
+  if (sl == 0) {
+    int t[kTop > 0 ? kTop : 1];
+    double v[kTop > 0 ? kTop : 1];
+#pragma unroll
+    for (int q = 0; q < kTop; q++) { t[q] = -1; v[q] = -1.0; }
+#pragma unroll 1
+    for (int q0 = 0; q0 < S; q0++) {
+      if (w.kmax[q0] == w.kmin[q0]) continue;
+      double vv = sw.pr[q0] * (w.kmax[q0] - w.kmin[q0]);
+      int tt = q0;
+#pragma unroll
+      for (int q = 0; q < kTop; q++) {
+        if (vv > v[q]) {
+          const double v2 = v[q]; const int t2 = t[q];
+          v[q] = vv; t[q] = tt; vv = v2; tt = t2;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kTop; q++) sw.top[q] = t[q];
+  }
+  __syncwarp(am);
+  const CostScalars cs{c.bo, c.batch, c.work, c.limit};
+  const double C = c.work / c.batch;
+  const bool grid = tau_hi > tau_lo;
+  double g_t = tau_lo, g_L = 0.0, g_d = 0.0;
+  if (grid) {
+    g_t = grid_point<MAXS>(tau_lo, tau_hi);
+    lb_cont<MAXS>(w, sw, S, c.bo, C, g_t, g_L, g_d, true);
+  }
+  {  // warm start: the 32 candidates of cand_prep, 16 per round
+    const double lmin = seg_min(grid ? g_L : 0.0);
+    const unsigned at = seg_ballot(grid && g_L == lmin);
+    const double tstar = __shfl_sync(am, g_t, base + (at ? __ffs(at) - 1 : 0));
+    int cstar = 0;
+    bool ok = false;
+    if (mine) {
+      const int lo = sw.kmi[r], chi = min(sw.kma[r], sw.gex[r]);
+      ok = grid && w.pre[r + 1] > w.pre[r] && chi >= lo;
+      if (ok) cstar = min(max(count_seeded(w.stage(r), w.row[r], tstar, lo, sw.kma[r]), lo), chi);
+    }
+    const unsigned lm = seg_ballot(ok);
+    const int nl = __popc(lm);
+    int sp = 0;
+#pragma unroll 1
+    for (int round = 0; round < 2; round++) {
+      const int vl = sl + 16 * round;   // the lane of cand_prep's 32-lane warm start
+      double tau = -inf;
+      int gen = -1;
+      if (nl > 0) {
+        const int li = vl % nl, k = vl / nl;
+        const int rr = __fns(lm, 0, li + 1);
+        const int cr = __shfl_sync(am, cstar, base + (rr & 15));
+        const int off = (k & 1) ? (k + 1) >> 1 : -(k >> 1);
+        const int mm = cr + off;
+        if (rr < S && mm >= sw.kmi[rr] && mm <= min(sw.kma[rr], sw.gex[rr])) {
+          gen = (rr << 16) | mm;
+          tau = __ldg(&HPS_TE(w.row[rr], mm - 1).et);
+        }
+      } else {
+        const int i = (int)(((long long)vl * n_cand) >> 5);
+        tau = cand_tau<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
+      }
+      if (tau >= tau_lo && tau <= tau_hi) eval_insert<MAXS>(cs, w, sw, S, tau, gen, buf);
+    }
+  }
+  const double ub = seg_min(buf.mn);
+  double ta = tau_lo, tbh = tau_hi;
+  if (grid && ub < inf) {
+    const double thr = (ub + 1e-15) * (1.0 + 1e-7);
+    interval_cells_half(g_t, g_L, g_d, thr, ta, tbh);
+#pragma unroll 1
+    for (int lvl = 1; lvl < HPS_GRID_LEVELS && ta <= tbh; lvl++) {
+      const double t1 = grid_point<MAXS>(ta, tbh);
+      double L1, d1;
+      lb_cont<MAXS>(w, sw, S, c.bo, C, t1, L1, d1, true);
+      interval_cells_half(t1, L1, d1, thr, ta, tbh);
+    }
+  }
+  if (mine) {
+    if (w.pre[r + 1] > w.pre[r]) {  // class leader with breakpoints
+      const int lo = sw.kmi[r], hi = sw.kma[r];
+      int alo = 0, an = 0;
+      const int chi = min(hi, sw.gex[r]);
+      if (ta <= tbh && chi >= lo) {
+        const int ma = count_seeded(w.stage(r), w.row[r], tbh, lo, hi);
+        const int mb = count_seeded(w.stage(r), w.row[r], ta, lo, hi);
+        alo = max(ma, lo);
+        an = max(0, min(mb, chi) - alo + 1);
+      }
+      sw.alo[r] = alo;
+      sw.an[r] = an;
+      sw.blo[r] = max(lo, sw.gex[r] + 1);
+    } else {
+      sw.alo[r] = 0;
+      sw.an[r] = 0;
+      sw.blo[r] = sw.kma[r] + 1;
+    }
+  }
+  __syncwarp(am);
+  return ub;
+}
+
+}  // namespace hps

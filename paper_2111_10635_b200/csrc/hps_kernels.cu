@@ -956,6 +956,7 @@ struct HpsInstance {
   uint64_t chunk = 0;     // plans per split-kernel chunk (HPS_CHUNK; 0: by MAXS)
   bool half_bisect = true;  // L <= 16: two plans per warp in the bisection (HPS_HALF_BISECT=0: one)
   bool half_stage = true;   // L <= 16: two plans per warp in the stage kernel (HPS_HALF_STAGE=0: one)
+  bool half_prep = true;    // L <= 16: two plans per warp in the prep kernel (HPS_HALF_PREP=0: one)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
 };
@@ -1245,6 +1246,75 @@ __device__ __forceinline__ void load_digits_half(const InstanceConsts& c, const 
     u128 part = 0;
     if (sl < L) part = (u128)(d & ((1 << src.tbits) - 1)) << ((L - 1 - sl) * src.tbits);
     rank = mk(seg_or_u64((uint64_t)(part >> 64)), seg_or_u64((uint64_t)part));
+  }
+}
+
+// prep_kernel with two plans per warp (L <= 16, hps_half.cuh)
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, HPS_CAND_MINB / WARPS)
+prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<16>* prep) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, sl = lane & 15;
+  const int v = warp * 2 + half;
+  WarpSmemL<16>& w = reinterpret_cast<WarpSmemL<16>*>(smem_raw)[v];
+  SweepSmem<16>& sw = reinterpret_cast<SweepSmem<16>*>(smem_raw + sizeof(WarpSmemL<16>) * WARPS * 2)[v];
+  StageBuf<16, false>& sb = reinterpret_cast<StageBuf<16, false>*>(
+      smem_raw + ((sizeof(WarpSmemL<16>) + sizeof(SweepSmem<16>)) * WARPS * 2 + 15) / 16 * 16)[v];
+  const PlanState<16>* states = reinterpret_cast<const PlanState<16>*>(cont.states);
+  const unsigned int n = *cont.count;
+  const uint64_t gh = ((uint64_t)blockIdx.x * WARPS + warp) * 2 + half, nh = (uint64_t)gridDim.x * WARPS * 2;
+  if (sl == 0) {
+    mbar_init(&sb.bar[0], 1);
+    mbar_init(&sb.bar[1], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  auto issue = [&](int slot, uint64_t q) {
+    if (sl == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&sb.bar[slot], sizeof(PlanState<16>));
+      bulk_g2s(&sb.ps[slot], states + q, sizeof(PlanState<16>), &sb.bar[slot]);
+    }
+  };
+  if (gh < n) issue(0, gh);
+  uint32_t it = 0;
+  for (uint64_t q = gh; q < n; q += nh, it++) {
+    const int slot = it & 1;
+    if (q + nh < n) issue(slot ^ 1, q + nh);
+    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
+    const PlanState<16>& ps = sb.ps[slot];
+    if (ps.n_cand >= 0) {   // (slow-path plans are finished elsewhere)
+      const int S = ps.S;
+      if (sl < S) {
+        const int e = ps.ent[sl];
+        const int type = __ldg(&tb.stages[e].type);
+        w.sp[sl] = tb.stages + e;
+        w.ent[sl] = e;
+        w.row[sl] = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
+        w.kmin[sl] = ps.kmin[sl];
+        w.kmax[sl] = ps.kmax[sl];
+        w.cls[sl] = tb_class(tb, e);
+        w.pre[sl] = ps.pre[sl];
+      }
+      if (sl == 0) w.pre[S] = ps.pre[S];
+      __syncwarp(seg_mask());
+      TieBuf buf;
+      buf.init();
+      const double ub = cand_prep_half<16>(c, tb, w, sw, S, ps.tau_lo, ps.tau_hi, ps.n_cand, buf);
+      PrepState<16>& out = prep[q];
+      if (sl < S) {
+        out.dom[sl] = (int8_t)sw.dom[sl];
+        out.lead[sl] = sw.lead[sl];
+        out.alo[sl] = (int16_t)sw.alo[sl];
+        out.an[sl] = (int16_t)sw.an[sl];
+        out.blo[sl] = (int16_t)sw.blo[sl];
+      }
+      if (sl == 0) {
+        out.ub = ub;
+        out.top = sw.top[0];
+      }
+    }
+    __syncwarp(seg_mask());
   }
 }
 
@@ -1557,6 +1627,10 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   auto kp = prep_kernel<MAXS, WARPS>;
   const size_t smemp = stage_offset<MAXS, WARPS>() + sizeof(StageBuf<MAXS, false>) * WARPS;
   CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemp));
+  auto kph = prep_kernel_h<WARPS>;
+  const size_t smemph = ((sizeof(WarpSmemL<16>) + sizeof(SweepSmem<16>)) * WARPS * 2 + 15) / 16 * 16 +
+                        sizeof(StageBuf<16, false>) * WARPS * 2;
+  if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(kph, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemph));
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
@@ -1578,7 +1652,11 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     }
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
-    kp<<<grid, WARPS * 32, smemp, st>>>(in->c, in->tb, cont, prep);
+    if (MAXS == 16 && in->half_prep) {   // two plans per warp (hps_half.cuh)
+      kph<<<grid, WARPS * 32, smemph, st>>>(in->c, in->tb, cont, reinterpret_cast<PrepState<16>*>(prep));
+    } else {
+      kp<<<grid, WARPS * 32, smemp, st>>>(in->c, in->tb, cont, prep);
+    }
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
     k2<<<grid, WARPS * 32, smem3, st>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
@@ -1781,6 +1859,7 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   if (const char* e = getenv("HPS_CARVEOUT")) in->carveout = std::min(100, atoi(e));
   if (const char* e = getenv("HPS_HALF_BISECT")) in->half_bisect = atoi(e) != 0;
   if (const char* e = getenv("HPS_HALF_STAGE")) in->half_stage = atoi(e) != 0;
+  if (const char* e = getenv("HPS_HALF_PREP")) in->half_prep = atoi(e) != 0;
   if (const char* e = getenv("HPS_CHUNK")) in->chunk = (uint64_t)std::max(1024ll, atoll(e));
   if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls

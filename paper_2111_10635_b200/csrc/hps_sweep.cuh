@@ -232,13 +232,14 @@ constexpr int kGrid = HPS_GRID;   // grid points per level of the interval searc
 // Returns L and a subgradient dL/dtau at tau.
 template <int MAXS, class W>
 __device__ __noinline__ void lb_cont(const W& w, const SweepSmem<MAXS>& sw, int S, double bo,
-                                        double C, double tau, double& L, double& dL) {
+                                        double C, double tau, double& L, double& dL, bool half = false) {
   // kGrid points per level: lanes p, p + kGrid, ... share point p and split the unpinned stages,
   // combined by butterfly steps; pinned stages contribute tau * p0 (slope p0), counted once.
   // A stage whose count one side decides on [tau_lo, tau_hi] (side_dominance) uses that side.
-  const int grp = (threadIdx.x & 31) / kGrid;
+  // half: one plan per 16 lanes (hps_half.cuh), each lane takes all stages of its point.
+  const int grp = half ? 0 : (threadIdx.x & 31) / kGrid, step = half ? 1 : 32 / kGrid;
   double P = (grp == 0) ? tau * sw.p0 : 0.0, dP = (grp == 0) ? sw.p0 : 0.0;
-  for (int j = grp; j < sw.nu; j += 32 / kGrid) {
+  for (int j = grp; j < sw.nu; j += step) {
     const int r = sw.ulist[j];
     const int dom = sw.dom[r];
     const double km = (double)sw.kmi[r];
@@ -262,10 +263,11 @@ __device__ __noinline__ void lb_cont(const W& w, const SweepSmem<MAXS>& sw, int 
     P += sw.pr[r] * v;
     dP += sw.pr[r] * dv;
   }
-  for (int o = kGrid; o < 32; o <<= 1) {
-    P += __shfl_xor_sync(0xffffffffu, P, o);
-    dP += __shfl_xor_sync(0xffffffffu, dP, o);
-  }
+  if (!half)
+    for (int o = kGrid; o < 32; o <<= 1) {
+      P += __shfl_xor_sync(0xffffffffu, P, o);
+      dP += __shfl_xor_sync(0xffffffffu, dP, o);
+    }
   L = C * P;
   dL = C * dP;
 }
