@@ -24,6 +24,7 @@ METRICS = {
 }
 AVERAGED = {"issue_active_pct", "threads_per_warp_inst", "fp64_pipe_pct"}
 SWEEP_KERNELS = ("stage_kernel", "bisect_kernel", "prep_kernel", "candidate_kernel", "slow_kernel",
+                 "stage_kernel_h", "bisect_kernel_h", "prep_kernel_h",
                  "finish_argmin", "merge_argmin")
 
 
@@ -42,7 +43,7 @@ def main():
         except ValueError:
             continue
         per[r[ii]][METRICS[r[mi]]] = v
-        names[r[ii]] = r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
+        names[r[ii]] = r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "").replace("hps::", "")
     agg = collections.defaultdict(lambda: collections.defaultdict(float))
     for lid, m in per.items():
         k = names[lid]
