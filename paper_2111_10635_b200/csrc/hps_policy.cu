@@ -171,14 +171,28 @@ __global__ void forward_kernel(PolicyDims d, PolicyBufs b, double temperature) {
   const int j = threadIdx.x;
   const int H = d.H, D = d.D, G4 = d.G4, T = d.T, DH = D + H;
   if (j < H) { h[j] = 0.0; c[j] = 0.0; }
+  // this thread's column of the hidden-state weights W_h stays in registers for all L steps
+  // (H <= 64; larger H reads it from global memory each step). Same FMA order either way.
+  constexpr int kRegH = 64;
+  double wh[kRegH];
+  const bool reg = H <= kRegH;
+#pragma unroll
+  for (int i = 0; i < kRegH; i++) wh[i] = (reg && j < G4 && i < H) ? b.w_cell[(long)(D + i) * G4 + j] : 0.0;
+  const double bj = (j < G4) ? b.b_cell[j] : 0.0;
   __syncthreads();
   for (int t = 0; t < d.L; t++) {
     // xh = concat(x_t, h)
     for (int k = j; k < DH; k += blockDim.x) b.xh[t * DH + k] = (k < D) ? b.feat[t * D + k] : h[k - D];
     if (j < G4) {  // z = xh @ W + b: hoisted x part (tensor cores) + h part
       double acc = b.xw[t * G4 + j];
-      for (int i = 0; i < H; i++) acc = fma(h[i], b.w_cell[(long)(D + i) * G4 + j], acc);
-      z[j] = acc + b.b_cell[j];
+      if (reg) {
+#pragma unroll
+        for (int i = 0; i < kRegH; i++)
+          if (i < H) acc = fma(h[i], wh[i], acc);
+      } else {
+        for (int i = 0; i < H; i++) acc = fma(h[i], b.w_cell[(long)(D + i) * G4 + j], acc);
+      }
+      z[j] = acc + bj;
     }
     __syncthreads();
     if (j < H) {
@@ -316,11 +330,9 @@ __global__ void __launch_bounds__(kRoundThreads) round_update_kernel(PolicyDims 
   __shared__ long redl[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const long G = in.G;
-  const int LT = d.L * d.T;
   double* R = b.scratch;           // rewards after winsorising
   double* X = b.scratch + G;       // R - baseline, then the gradient weights
   double* W = b.scratch + 2 * G;   // squared deviations
-  double* TERM = b.scratch + 4 * G;  // [L*T][G] dlogits terms
   const double base = b.state[0];
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   const int round = (in.round > 0) ? in.round : (int)b.ctr[0];
@@ -388,22 +400,6 @@ __global__ void __launch_bounds__(kRoundThreads) round_update_kernel(PolicyDims 
     X[g] = (r2 - base) * scale;
   }
   __syncthreads();
-  // dlogits terms (weight * (onehot - probs)) / temperature, all (t, a, g) in parallel
-  for (long q = tid; q < (long)LT * G; q += nt) {
-    const int e = (int)(q / G);
-    const long g = q - (long)e * G;
-    const int t = e / d.T, a = e - t * d.T;
-    const double oh = (in.plans[g * d.L + t] == a) ? 1.0 : 0.0;
-    TERM[q] = X[g] * (oh - b.probs[e]) / in.temperature;
-  }
-  __syncthreads();
-  // accumulated in trace order (training.py:134-143): dlogits += term_g, g = 0, 1, ...
-  for (int e = tid; e < LT; e += nt) {
-    const double* row = TERM + (long)e * G;
-    double acc = 0.0;
-    for (long g = 0; g < G; g++) acc = acc + row[g];
-    b.dlogits[e] = acc;
-  }
   const double mean_cost = block_pairwise(in.cost, G, b.pw_leaf, b.pw_val, &sh[3]) / (double)G;
   if (tid == 0) {
     const double nb = (1.0 - in.gamma) * base + in.gamma * mean_r;
@@ -416,6 +412,32 @@ __global__ void __launch_bounds__(kRoundThreads) round_update_kernel(PolicyDims 
     b.ctr[0] = (unsigned long long)round + 1;   // device round counter (graph-replayed rounds)
     b.ctr[1] += (unsigned long long)G * d.L;
   }
+}
+
+// dlogits[t][a] = sum over traces g (in order) of (w_g * (onehot_g - p) / temperature)
+// (training.py:134-143). One block per (t, a): the terms of a chunk of traces are formed in
+// parallel in shared memory, then one thread adds them in trace order (the reference's
+// `dlogits += ...` accumulation, starting from zeros).
+constexpr int kDlChunk = 4096;
+__global__ void dlogits_kernel(PolicyDims d, PolicyBufs b, const uint8_t* plans, long G, double temperature) {
+  __shared__ double terms[kDlChunk];
+  const int e = blockIdx.x, t = e / d.T, a = e - t * d.T;
+  const double p = b.probs[e];
+  const double* X = b.scratch + G;   // gradient weights (round_update_kernel)
+  double acc = 0.0;
+  for (long g0 = 0; g0 < G; g0 += kDlChunk) {
+    const int n = (int)min((long)kDlChunk, G - g0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const long g = g0 + i;
+      const double oh = (plans[g * d.L + t] == a) ? 1.0 : 0.0;
+      terms[i] = X[g] * (oh - p) / temperature;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < n; i++) acc = acc + terms[i];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) b.dlogits[e] = acc;
 }
 
 __global__ void set_ctr_kernel(unsigned long long* ctr, unsigned long long round, unsigned long long draws) {
@@ -579,7 +601,7 @@ int hps_policy_create(int32_t L, int32_t D, int32_t H, int32_t T, int32_t lstm, 
   for (double** q : {&b.gi, &b.gf, &b.go, &b.gg, &b.cc, &b.cp, &b.tc, &b.hh}) rc |= palloc(p, q, (size_t)L * H);
   rc |= palloc(p, &b.probs, (size_t)L * T);     rc |= palloc(p, &b.cdf, (size_t)L * T);
   rc |= palloc(p, &b.dlogits, (size_t)L * T);
-  rc |= palloc(p, &b.scratch, (size_t)max_plans * (4 + (size_t)L * T));
+  rc |= palloc(p, &b.scratch, (size_t)max_plans * 4);
   rc |= palloc(p, &b.state, 16);                rc |= palloc(p, &b.flags, 4);
   rc |= palloc(p, &b.dz, (size_t)L * G4);       rc |= palloc(p, &b.ctr, 2);
   rc |= palloc(p, &b.pw_leaf, (size_t)2 * (max_plans / 64 + 4));
@@ -661,6 +683,9 @@ int hps_policy_reinforce(HpsPolicy* p, const double* d_cost, const uint8_t* d_st
   RoundIn in{d_cost, d_status, d_plans, G, temperature, lr, gamma, round, d_history, d_best_plan, d_best_where};
   HPS_COUNT_LAUNCH();
   round_update_kernel<<<1, kRoundThreads, 0, st>>>(p->d, p->b, in);
+  PCUDA(cudaGetLastError());
+  HPS_COUNT_LAUNCH();
+  dlogits_kernel<<<p->d.L * p->d.T, 256, 0, st>>>(p->d, p->b, d_plans, G, temperature);
   PCUDA(cudaGetLastError());
   const size_t smem = sizeof(double) * (3 * p->d.H + p->d.G4);
   HPS_COUNT_LAUNCH();
