@@ -1025,8 +1025,16 @@ __host__ __device__ constexpr size_t stage_offset() {
   return ((sizeof(WarpSmemL<MAXS>) + sizeof(SweepSmem<MAXS>)) * WARPS + 15) / 16 * 16;
 }
 
+// staged only for MAXS <= 16: the 64-stage records (1 KB + 0.5 KB, double-buffered) would cost
+// more occupancy (shared memory) than the staging saves
+template <int MAXS>
+__host__ __device__ constexpr bool staged() { return MAXS <= 16; }
+template <int MAXS, bool PREP>
+__host__ __device__ constexpr size_t stage_bytes() { return staged<MAXS>() ? sizeof(StageBuf<MAXS, PREP>) : 0; }
+
 template <int MAXS, bool PREP>
 __device__ __forceinline__ void stage_init(StageBuf<MAXS, PREP>& sb) {
+  if (!staged<MAXS>()) return;
   if ((threadIdx.x & 31) == 0) {
     mbar_init(&sb.bar[0], 1);
     mbar_init(&sb.bar[1], 1);
@@ -1040,7 +1048,7 @@ __device__ __forceinline__ void stage_init(StageBuf<MAXS, PREP>& sb) {
 template <int MAXS, bool PREP>
 __device__ __forceinline__ void stage_issue(StageBuf<MAXS, PREP>& sb, int slot, const PlanState<MAXS>* states,
                                             const PrepState<MAXS>* prep, uint64_t q) {
-  if ((threadIdx.x & 31) == 0) {
+  if (staged<MAXS>() && (threadIdx.x & 31) == 0) {
     fence_proxy_async_smem();
     const uint32_t bytes = sizeof(PlanState<MAXS>) + (PREP ? sizeof(PrepState<MAXS>) : 0);
     mbar_arrive_expect_tx(&sb.bar[slot], bytes);
@@ -1154,8 +1162,8 @@ bisect_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, Pending 
   for (uint64_t q = gw; q < n; q += nw, it++) {
     const int slot = it & 1;
     if (q + nw < n) stage_issue(sb, slot ^ 1, states, (const PrepState<MAXS>*)nullptr, q + nw);
-    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
-    const PlanState<MAXS>& ps = sb.ps[slot];   // staged copy; results go to states[q]
+    if (staged<MAXS>()) mbar_wait(&sb.bar[slot], (it >> 1) & 1);
+    const PlanState<MAXS>& ps = staged<MAXS>() ? sb.ps[slot] : states[q];   // results go to states[q]
     PlanState<MAXS>& out = states[q];
     const int S = ps.S;
 #pragma unroll 1
@@ -1440,8 +1448,8 @@ prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<
   for (uint64_t q = gw; q < n; q += nw, it++) {
     const int slot = it & 1;
     if (q + nw < n) stage_issue(sb, slot ^ 1, states, (const PrepState<MAXS>*)nullptr, q + nw);
-    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
-    const PlanState<MAXS>& ps = sb.ps[slot];
+    if (staged<MAXS>()) mbar_wait(&sb.bar[slot], (it >> 1) & 1);
+    const PlanState<MAXS>& ps = staged<MAXS>() ? sb.ps[slot] : states[q];
     if (ps.n_cand < 0) { __syncwarp(); continue; }  // slow path
     load_state<MAXS>(c, tb, ps, w);
     const int S = ps.S;
@@ -1480,7 +1488,7 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
   StageBuf<MAXS, true>& sb = reinterpret_cast<StageBuf<MAXS, true>*>(
       smem_raw + stage_offset<MAXS, WARPS>())[warp];
   CandQueue* queues = reinterpret_cast<CandQueue*>(smem_raw + stage_offset<MAXS, WARPS>() +
-                                                   sizeof(StageBuf<MAXS, true>) * WARPS);
+                                                   stage_bytes<MAXS, true>() * WARPS);
   if (lane == 0) sw.cq = &queues[warp];
   const unsigned int n = *cont.count;
   Key best;
@@ -1495,12 +1503,12 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
   for (uint64_t q = gw; q < n; q += nw, it++) {
     const int slot = it & 1;
     if (q + nw < n) stage_issue(sb, slot ^ 1, states, prep, q + nw);
-    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
-    const PlanState<MAXS>& ps = sb.ps[slot];
+    if (staged<MAXS>()) mbar_wait(&sb.bar[slot], (it >> 1) & 1);
+    const PlanState<MAXS>& ps = staged<MAXS>() ? sb.ps[slot] : states[q];
     if (ps.n_cand < 0) { __syncwarp(); continue; }  // slow path
     load_state<MAXS>(c, tb, ps, w);
     const int S = ps.S;
-    const PrepState<MAXS>& pp = sb.pp[slot];
+    const PrepState<MAXS>& pp = staged<MAXS>() ? sb.pp[slot] : prep[q];
 #pragma unroll 1
     for (int r = lane; r < S; r += 32) {
       const int lo = ps.kmin[r], hi = ps.kmax[r];
@@ -1617,15 +1625,15 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(buf + 256 + state_bytes);
   KeyPart* parts_a = parts;
   KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
-  const size_t smem3 = stage_offset<MAXS, WARPS>() + (sizeof(StageBuf<MAXS, true>) + sizeof(CandQueue)) * WARPS;
-  const size_t smem1 = (sizeof(WarpSmemL<MAXS>) * WARPS + 15) / 16 * 16 + sizeof(StageBuf<MAXS, false>) * WARPS;
+  const size_t smem3 = stage_offset<MAXS, WARPS>() + (stage_bytes<MAXS, true>() + sizeof(CandQueue)) * WARPS;
+  const size_t smem1 = (sizeof(WarpSmemL<MAXS>) * WARPS + 15) / 16 * 16 + stage_bytes<MAXS, false>() * WARPS;
   auto kb = bisect_kernel<MAXS, WARPS>;
   CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
   auto kbh = bisect_kernel_h<WARPS>;
   const size_t smemh = (sizeof(WarpSmemL<16>) * WARPS * 2 + 15) / 16 * 16 + sizeof(StageBuf<16, false>) * WARPS * 2;
   if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(kbh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemh));
   auto kp = prep_kernel<MAXS, WARPS>;
-  const size_t smemp = stage_offset<MAXS, WARPS>() + sizeof(StageBuf<MAXS, false>) * WARPS;
+  const size_t smemp = stage_offset<MAXS, WARPS>() + stage_bytes<MAXS, false>() * WARPS;
   CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemp));
   auto kph = prep_kernel_h<WARPS>;
   const size_t smemph = ((sizeof(WarpSmemL<16>) + sizeof(SweepSmem<16>)) * WARPS * 2 + 15) / 16 * 16 +

@@ -13,7 +13,7 @@ from paper_2111_10635_b200.model import JobParams
 g, c, lim = load_fixture("cfg5")
 inst = DeviceInstance(g, c, JobParams(lim))
 pcg = pcg_from_generator(np.random.default_rng(0))
-n = 1 << 18
+n = int(os.environ.get("CFG5_N", 1 << 18))
 stats = "stats" in os.environ.get("HPS_LIBRARY", "")
 lib = _abi.load_library()
 buf = (C.c_ulonglong * 24)()
