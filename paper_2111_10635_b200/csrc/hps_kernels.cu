@@ -1266,31 +1266,13 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
   const int v = warp * 2 + half;
   WarpSmemL<16>& w = reinterpret_cast<WarpSmemL<16>*>(smem_raw)[v];
   SweepSmem<16>& sw = reinterpret_cast<SweepSmem<16>*>(smem_raw + sizeof(WarpSmemL<16>) * WARPS * 2)[v];
-  StageBuf<16, false>& sb = reinterpret_cast<StageBuf<16, false>*>(
-      smem_raw + ((sizeof(WarpSmemL<16>) + sizeof(SweepSmem<16>)) * WARPS * 2 + 15) / 16 * 16)[v];
   const PlanState<16>* states = reinterpret_cast<const PlanState<16>*>(cont.states);
   const unsigned int n = *cont.count;
   const uint64_t gh = ((uint64_t)blockIdx.x * WARPS + warp) * 2 + half, nh = (uint64_t)gridDim.x * WARPS * 2;
-  if (sl == 0) {
-    mbar_init(&sb.bar[0], 1);
-    mbar_init(&sb.bar[1], 1);
-    mbar_init_fence();
-  }
-  __syncwarp();
-  auto issue = [&](int slot, uint64_t q) {
-    if (sl == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&sb.bar[slot], sizeof(PlanState<16>));
-      bulk_g2s(&sb.ps[slot], states + q, sizeof(PlanState<16>), &sb.bar[slot]);
-    }
-  };
-  if (gh < n) issue(0, gh);
-  uint32_t it = 0;
-  for (uint64_t q = gh; q < n; q += nh, it++) {
-    const int slot = it & 1;
-    if (q + nh < n) issue(slot ^ 1, q + nh);
-    mbar_wait(&sb.bar[slot], (it >> 1) & 1);
-    const PlanState<16>& ps = sb.ps[slot];
+  // (no shared-memory staging of the plan states here: two plan views per warp already take
+  // the shared memory, and the L1 is worth more to this kernel's table loads)
+  for (uint64_t q = gh; q < n; q += nh) {
+    const PlanState<16>& ps = states[q];
     if (ps.n_cand >= 0) {   // (slow-path plans are finished elsewhere)
       const int S = ps.S;
       if (sl < S) {
@@ -1636,8 +1618,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   const size_t smemp = stage_offset<MAXS, WARPS>() + stage_bytes<MAXS, false>() * WARPS;
   CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemp));
   auto kph = prep_kernel_h<WARPS>;
-  const size_t smemph = ((sizeof(WarpSmemL<16>) + sizeof(SweepSmem<16>)) * WARPS * 2 + 15) / 16 * 16 +
-                        sizeof(StageBuf<16, false>) * WARPS * 2;
+  const size_t smemph = (sizeof(WarpSmemL<16>) + sizeof(SweepSmem<16>)) * WARPS * 2;
   if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(kph, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemph));
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
