@@ -9,6 +9,10 @@
 // cands_prefix (hps_eval.cuh), so the same bits.
 #pragma once
 
+#ifndef HPS_HALF_BISECT_STAGED
+#define HPS_HALF_BISECT_STAGED 1   // bulk-copy staging of the plan states in bisect_kernel_h
+#endif
+
 namespace hps {
 
 // the 16 lanes of this thread's half: every collective below names exactly its segment (the two
@@ -183,11 +187,12 @@ bisect_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, Pendin
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, sl = lane & 15;
   WarpSmemL<16>& w = reinterpret_cast<WarpSmemL<16>*>(smem_raw)[warp * 2 + half];
-  StageBuf<16, false>& sb =
-      reinterpret_cast<StageBuf<16, false>*>(smem_raw + (sizeof(WarpSmemL<16>) * WARPS * 2 + 15) / 16 * 16)[warp * 2 + half];
   PlanState<16>* states = reinterpret_cast<PlanState<16>*>(cont.states);
   const unsigned int n = *cont.count;
   const uint64_t gh = ((uint64_t)blockIdx.x * WARPS + warp) * 2 + half, nh = (uint64_t)gridDim.x * WARPS * 2;
+#if HPS_HALF_BISECT_STAGED
+  StageBuf<16, false>& sb =
+      reinterpret_cast<StageBuf<16, false>*>(smem_raw + (sizeof(WarpSmemL<16>) * WARPS * 2 + 15) / 16 * 16)[warp * 2 + half];
   if (sl == 0) {
     mbar_init(&sb.bar[0], 1);
     mbar_init(&sb.bar[1], 1);
@@ -202,12 +207,17 @@ bisect_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, Pendin
     }
   };
   if (gh < n) issue(0, gh);
+#endif
   uint32_t it = 0;
   for (uint64_t q = gh; q < n; q += nh, it++) {
+#if HPS_HALF_BISECT_STAGED
     const int slot = it & 1;
     if (q + nh < n) issue(slot ^ 1, q + nh);
     mbar_wait(&sb.bar[slot], (it >> 1) & 1);
     const PlanState<16>& ps = sb.ps[slot];
+#else
+    const PlanState<16>& ps = states[q];   // (copied to registers/shared below before `out` is written)
+#endif
     PlanState<16>& out = states[q];
     const int S = ps.S;
     if (sl < S) {
