@@ -543,3 +543,217 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
 }
 
 }  // namespace hps
+
+namespace hps {
+
+// per-plan view of candidate_kernel_h (S <= 16): exactly what cost_exact, cand_tau2, the filter and
+// the final counts read, packed so that eight blocks of four warps (16 plans) fit the 132 KB
+// shared-memory configuration and leave the rest of the SM's 256 KB to the L1 (table loads).
+// It serves as both the plan view (row) and the sweep constants of the shared helpers.
+struct CandView {
+  const TEPair* row[16];
+  double pr[16];       // price per second of stage r's type
+  double etp[16];      // et at the pinned count (kmin == kmax)
+  float est[16][6];    // count_est seeds; a side off per side_dominance is {0, -1, 0}
+  float fpr[16];
+  int32_t kmi[16], kma[16];
+  int32_t pre2[17];
+  int32_t top;
+  int16_t alo[16], an[16], blo[16];
+  int8_t lead[16], type[16];
+  uint32_t tsum[kMaxT];
+};
+
+// count_lb32 (hps_sweep.cuh) from the count_est seeds: they hold the same FP32 side constants, with
+// the sides count_lb32 skips (dominated, rb == 0 or frac == 0) set to rb = 0
+__device__ __forceinline__ int count_lb32_est(const float* e, float tau) {
+  float lo = 1.0f;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const float rb = e[3 * side], omf = e[3 * side + 1], frac = e[3 * side + 2];
+    if (rb == 0.0f) continue;
+    const float B = tau * rb;
+    const float h = B - omf;
+    if (!(h > 1e-3f * B)) continue;
+    const float rh = rcp_approx_f32(h);
+    const float ee = 4e-7f * (B * rh + 2.0f) + 1e-6f;
+    lo = fmaxf(lo, (frac * rh) * (1.0f - ee));
+  }
+  return (int)ceilf(lo);
+}
+
+// overflow_pass (hps_sweep.cuh) for the plan of this half: candidates strided over 16 lanes
+__device__ __noinline__ double overflow_pass_half(const CostScalars cs, const CandView& v, int S, double tau_lo,
+                                                  double tau_hi, int n2, double lim) {
+  double bt = -__longlong_as_double(0x7ff0000000000000LL);
+  int sp = 0;
+  for (int i = (threadIdx.x & 15); i < n2; i += 16) {
+    int gen;
+    const double tau = cand_tau2<16>(v, v, i, sp, tau_lo, tau_hi, gen);
+    if (!(tau >= tau_lo && tau <= tau_hi) || !(tau > bt)) continue;
+    if (cost_exact<16>(cs, v, v, S, tau, gen) <= lim) bt = tau;
+  }
+  return bt;
+}
+
+// cand_main (hps_sweep.cuh) for the plan of this half (S <= 16): filter rounds of 16 candidates,
+// survivors compacted into this half's 32 slots of the warp's queue and evaluated 16 at a time.
+// The FP32 bound sums in another order than the 32-lane version; the filter's 1e-5 slack covers
+// that (a skipped candidate still costs more than the minimum + 1e-15), so the result is the same.
+__device__ double cand_main_half(const InstanceConsts& c, CandView& v, CandQueue& cq, int S, double tau_lo,
+                                 double tau_hi, double ub, TieBuf& buf) {
+  const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
+  const unsigned am = seg_mask();
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const CostScalars cs{c.bo, c.batch, c.work, c.limit};
+  // restricted_prefix over the segment
+  const int cnt = (sl < S) ? v.an[sl] + max(0, v.kma[sl] - v.blo[sl] + 1) : 0;
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const int u = __shfl_up_sync(am, inc, o);
+    if (sl >= o) inc += u;
+  }
+  const int tot = __shfl_sync(am, inc, base + 15);
+  if (sl < S) v.pre2[sl] = inc - cnt;
+  if (sl == 0) v.pre2[S] = tot;
+  __syncwarp(am);
+  const int n2 = 2 + tot;
+#ifdef HPS_STATS
+  if (sl == 0) {
+    HPS_STAT(ST_N2, n2);
+    int unc = 0;
+    for (int r = 0; r < S; r++) unc += max(0, v.kma[r] - v.blo[r] + 1);
+    HPS_STAT(ST_UNCERT, unc);
+  }
+#endif
+  const float fC = (float)(c.work / c.batch);
+  const float pl0 = seg_sumf((sl < S) ? v.fpr[sl] * (float)v.kmi[sl] : 0.0f);  // sum of pr count(tau_hi)
+  const int top = v.top;
+  double* qt = cq.q + 2 * base;      // this half's 32 queue slots
+  int32_t* qg = cq.qg + 2 * base;
+  int sp = 0, qn = 0;
+  const unsigned lt = (1u << sl) - 1u;
+  const int rounds = (n2 + 15) >> 4;
+  for (int jr = 0; jr < rounds; jr++) {
+    const int i = jr * 16 + sl;
+    double tau = 0.0;
+    int gen = -1;
+    bool keep = false;
+    if (i < n2) {
+      tau = cand_tau2<16>(v, v, i, sp, tau_lo, tau_hi, gen);
+      keep = tau >= tau_lo && tau <= tau_hi;
+      if (keep && gen >= 0) {
+        const int g = gen >> 16, m = gen & 0xffff;
+        const float tf = (float)tau;
+        float P = pl0 + v.fpr[g] * (float)(m - v.kmi[g]);
+        if (top >= 0 && top != g) {
+          const int d = count_lb32_est(v.est[top], tf) - v.kmi[top];
+          if (d > 0) P += v.fpr[top] * (float)d;
+        }
+        keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > ub + 1e-15);
+      }
+    }
+    const unsigned mk = seg_ballot(keep);
+    if (keep) { qt[qn + __popc(mk & lt)] = tau; qg[qn + __popc(mk & lt)] = gen; }
+    qn += __popc(mk);
+    __syncwarp(am);
+    if (qn >= 16) {
+      const double t = qt[qn - 16 + sl];
+      const int tg = qg[qn - 16 + sl];
+      HPS_STAT(ST_CANDS, 1);
+      eval_insert<16>(cs, v, v, S, t, tg, buf);
+      qn -= 16;
+      ub = fmin(ub, seg_min(buf.mn));
+      __syncwarp(am);
+    }
+  }
+  if (sl < qn) {
+    HPS_STAT(ST_CANDS, 1);
+    eval_insert<16>(cs, v, v, S, qt[sl], qg[sl], buf);
+  }
+  const double mf = seg_min(buf.mn);
+  if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
+  const double lim = mf + 1e-15;
+  double bt;
+  if (seg_ballot(buf.overflow)) {  // rare: exact second pass with the final limit
+    bt = overflow_pass_half(cs, v, S, tau_lo, tau_hi, n2, lim);
+  } else {
+    bt = buf.best_tau(lim);
+  }
+  return seg_max(bt);
+}
+
+// phase_final_fast (hps_eval.cuh) for the plan of this half: counts at tau (segment lane sl keeps
+// stage sl's in k), add_ps_cores, cost
+__device__ void final_half(const InstanceConsts& c, CandView& v, const StageEntry* st, int S, double tau,
+                           PlanOut& out, int& k) {
+  const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
+  const unsigned am = seg_mask();
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  int accel = 0, on_ps = 0, t = -1;
+  double emax = 0.0;
+  k = 0;
+  if (sl < S) {
+    const int lo = v.kmi[sl], hi = v.kma[sl];
+    k = (lo == hi) ? lo : count_seeded(*st, v.row[sl], tau, lo, hi);
+    t = v.type[sl];
+    if (!c.is_cpu[t]) accel = k;
+    if (t == c.ps_type) on_ps = k;
+    emax = __ldg(&HPS_TE(v.row[sl], k - 1).et);
+  }
+  accel = seg_sum(accel);
+  on_ps = seg_sum(on_ps);
+  emax = seg_max(emax);
+  int ps = 0;
+  if (c.with_ps && accel != 0) {
+    if (c.ps_type < 0) { out.status = HPS_ST_NO_CPU_TYPE; out.cost = __longlong_as_double(0x7ff8000000000000LL); out.gap = 0; return; }
+    ps = (int)ceil(c.ps_cores_per_gpu * (double)accel - 1e-9);
+    const long long would = (long long)on_ps + ps;
+    if (would > c.quota[c.ps_type]) {
+      out.status = HPS_ST_PS_QUOTA;
+      out.gap = clamp_gap((double)(would - c.quota[c.ps_type]) / (double)c.quota[c.ps_type]);
+      out.cost = c.penalty_scale * (1.0 + pmax(0.0, out.gap));
+      return;
+    }
+  }
+  // evaluate(): overall = B / max_s et_s; zero-time stages give inf (ls/costmodel.py:127-128)
+  const double overall = (emax > 0) ? c.batch / emax : inf;
+  const double exec_time = (overall > 0 && overall != inf) ? c.work / overall : 0.0;
+  // per-type totals, summed over types in order of first occurrence, then the PS type
+  unsigned rem = seg_or(t >= 0 ? 1u << t : 0u);
+  while (rem) {
+    const int ty = __ffs(rem) - 1;
+    rem &= rem - 1;
+    const int tot = seg_sum(t == ty ? k : 0);
+    if (sl == 0) v.tsum[ty] = (unsigned)tot;
+  }
+  __syncwarp(am);
+  double cost = 0.0;
+  if (sl == 0) {
+    double per_second = 0.0;
+    unsigned seen = 0;
+    bool first = true;
+#pragma unroll 1
+    for (int s = 0; s < S; s++) {
+      const int ty = v.type[s];
+      if (seen >> ty & 1u) continue;
+      seen |= 1u << ty;
+      const double term = c.price_s[ty] * (double)(v.tsum[ty] + (ty == c.ps_type ? (unsigned long long)ps : 0ull));
+      per_second = first ? term : per_second + term;
+      first = false;
+    }
+    if (ps > 0 && !(seen >> c.ps_type & 1u)) {
+      const double term = c.price_s[c.ps_type] * (double)ps;
+      per_second = first ? term : per_second + term;
+    }
+    cost = exec_time * per_second;
+  }
+  out.cost = __shfl_sync(am, cost, base);
+  out.status = HPS_ST_OK;
+  out.gap = 0.0;
+  out.ps = ps;
+}
+
+}  // namespace hps
+

@@ -957,6 +957,7 @@ struct HpsInstance {
   bool half_bisect = true;  // L <= 16: two plans per warp in the bisection (HPS_HALF_BISECT=0: one)
   bool half_stage = true;   // L <= 16: two plans per warp in the stage kernel (HPS_HALF_STAGE=0: one)
   bool half_prep = true;    // L <= 16: two plans per warp in the prep kernel (HPS_HALF_PREP=0: one)
+  bool half_cand = true;    // L <= 16: two plans per warp in the candidate kernel (HPS_HALF_CAND=0: one)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
 };
@@ -1308,6 +1309,116 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
   }
 }
 
+// candidate_kernel with two plans per warp (L <= 16, hps_half.cuh): each half fills its CandView
+// (segment lane sl: stage sl) and shares the warp's survivor queue (32 slots per half)
+template <int WARPS, bool ARGMIN>
+__global__ void __launch_bounds__(WARPS * 32, HPS_CAND_MINB / WARPS)
+candidate_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, const PrepState<16>* prep, Outputs o,
+                   int feasible_only, KeyPart* parts, int first) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, sl = lane & 15;
+  CandView& v = reinterpret_cast<CandView*>(smem_raw)[warp * 2 + half];
+  CandQueue& cq = reinterpret_cast<CandQueue*>(smem_raw + sizeof(CandView) * WARPS * 2)[warp];
+  const PlanState<16>* states = reinterpret_cast<const PlanState<16>*>(cont.states);
+  const unsigned int n = *cont.count;
+  const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp;
+  const uint64_t gh = gw * 2 + half, nh = (uint64_t)gridDim.x * WARPS * 2;
+  const unsigned am = seg_mask();
+  Key best;
+  best.cost = __longlong_as_double(0x7ff0000000000000LL);
+  best.hi = best.lo = ~0ull;
+  best.status = 0;
+  unsigned long long feas = 0;
+  uint32_t flags = 0;
+  for (uint64_t q = gh; q < n; q += nh) {
+    const PlanState<16>& ps = states[q];
+    if (ps.n_cand < 0) { __syncwarp(am); continue; }  // slow path
+    const int S = ps.S;
+    const PrepState<16>& pp = prep[q];
+    const StageEntry* st = nullptr;
+    if (sl < S) {
+      const int e = ps.ent[sl];
+      st = tb.stages + e;
+      const int type = __ldg(&st->type);
+      const int lo = ps.kmin[sl], hi = ps.kmax[sl];
+      const TEPair* row = tb.te + c.te_off[type] + (int64_t)(e - type * c.P) * (int64_t)(c.et_cap[type] + 1);
+      v.row[sl] = row;
+      v.type[sl] = (int8_t)type;
+      v.pr[sl] = c.price_s[type];
+      v.fpr[sl] = (float)c.price_s[type];
+      v.kmi[sl] = lo;
+      v.kma[sl] = hi;
+      v.etp[sl] = (lo == hi) ? __ldg(&HPS_TE(row, lo - 1).et) : 0.0;
+      const int dom = pp.dom[sl];
+#pragma unroll
+      for (int side = 0; side < 2; side++) {   // est_setup (hps_sweep.cuh)
+        const float rb = __ldg(side ? &st->f_rbd : &st->f_rbo);
+        const float frac = __ldg(side ? &st->f_beta : &st->f_alpha);
+        const bool on = (dom != 2 - side) && rb != 0.0f && frac != 0.0f;
+        v.est[sl][3 * side + 0] = on ? rb : 0.0f;
+        v.est[sl][3 * side + 1] = on ? __ldg(side ? &st->f_omb : &st->f_oma) : -1.0f;
+        v.est[sl][3 * side + 2] = on ? frac : 0.0f;
+      }
+      v.lead[sl] = pp.lead[sl];
+      v.alo[sl] = pp.alo[sl];
+      v.an[sl] = pp.an[sl];
+      v.blo[sl] = pp.blo[sl];
+    }
+    if (sl == 0) v.top = pp.top;
+    __syncwarp(am);
+    PlanOut r;
+    r.ps = 0;
+    r.gap = 0.0;
+    r.S = S;
+    TieBuf buf;
+    buf.init();
+    const double tau = cand_main_half(c, v, cq, S, ps.tau_lo, ps.tau_hi, pp.ub, buf);
+    int k = 0;
+    if (tau != tau) {
+      r.status = HPS_ST_NO_CANDIDATE;
+      r.gap = 1.0;
+      r.cost = c.penalty_scale * (1.0 + 1.0);
+    } else {
+      final_half(c, v, st, S, tau, r, k);
+    }
+    if (!ARGMIN) {   // write_plan for this half's plan
+      const bool ok = (r.status & 0x7f) == HPS_ST_OK;
+      const bool counts = ok || (r.status & 0x7f) == HPS_ST_PS_QUOTA;
+      const uint64_t p = ps.p;
+      if (sl == 0) {
+        o.cost[p] = r.cost;
+        o.status[p] = (uint8_t)r.status;
+        if (o.gap) o.gap[p] = r.gap;
+        if (o.ps) o.ps[p] = ok ? r.ps : 0;
+        if (o.num_stages) o.num_stages[p] = r.S;
+      }
+      if (o.k && sl < c.L) o.k[p * (uint64_t)c.L + sl] = (counts && sl < r.S) ? (int32_t)k : 0;
+    } else {
+      const int code = r.status & 0x7f;
+      if (code == HPS_ST_OK) feas++;
+      if (code == HPS_ST_NO_CPU_TYPE) flags |= 1u;
+      const bool take = feasible_only ? (code == HPS_ST_OK) : (code != HPS_ST_NO_CPU_TYPE && code != HPS_ST_INVALID);
+      if (take) {
+        Key kk{r.cost, ps.rank_hi, ps.rank_lo, (uint32_t)r.status};
+        if (key_less(kk, best)) best = kk;
+      }
+    }
+    __syncwarp(am);
+  }
+  if (ARGMIN) {   // the two halves' partials meet, lane 0 writes the warp's
+    __syncwarp();
+    Key ob;
+    ob.cost = __shfl_xor_sync(0xffffffffu, best.cost, 16);
+    ob.hi = __shfl_xor_sync(0xffffffffu, best.hi, 16);
+    ob.lo = __shfl_xor_sync(0xffffffffu, best.lo, 16);
+    ob.status = __shfl_xor_sync(0xffffffffu, best.status, 16);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 16);
+    feas += __shfl_xor_sync(0xffffffffu, feas, 16);
+    if (key_less(ob, best)) best = ob;
+    if (lane == 0) merge_part(parts, gw, first, best, feas, flags);
+  }
+}
+
 // stage_kernel with two plans per warp (L <= 16, hps_half.cuh)
 template <int WARPS, bool ARGMIN, int SRC>
 __global__ void __launch_bounds__(WARPS * 32, HPS_STAGE_MINB / WARPS)
@@ -1622,6 +1733,10 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(kph, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemph));
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  auto k2h = candidate_kernel_h<WARPS, ARGMIN>;
+  const size_t smem2h = sizeof(CandView) * WARPS * 2 + sizeof(CandQueue) * WARPS;
+  if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(k2h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2h));
+  if (MAXS == 16 && in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2h, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
   if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
   for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
     const uint64_t c1 = std::min(n, c0 + chunk);
@@ -1648,7 +1763,12 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
     }
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
-    k2<<<grid, WARPS * 32, smem3, st>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
+    if (MAXS == 16 && in->half_cand) {   // two plans per warp (hps_half.cuh)
+      k2h<<<grid, WARPS * 32, smem2h, st>>>(in->c, in->tb, cont, reinterpret_cast<const PrepState<16>*>(prep), o,
+                                            feasible_only, parts_b, first);
+    } else {
+      k2<<<grid, WARPS * 32, smem3, st>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
+    }
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaFreeAsync(buf, st));
@@ -1849,6 +1969,7 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   if (const char* e = getenv("HPS_HALF_BISECT")) in->half_bisect = atoi(e) != 0;
   if (const char* e = getenv("HPS_HALF_STAGE")) in->half_stage = atoi(e) != 0;
   if (const char* e = getenv("HPS_HALF_PREP")) in->half_prep = atoi(e) != 0;
+  if (const char* e = getenv("HPS_HALF_CAND")) in->half_cand = atoi(e) != 0;
   if (const char* e = getenv("HPS_CHUNK")) in->chunk = (uint64_t)std::max(1024ll, atoll(e));
   if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls

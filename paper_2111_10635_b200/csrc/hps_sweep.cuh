@@ -76,8 +76,8 @@ __device__ __forceinline__ void est_setup(const W& w, SweepSmem<MAXS>& sw, int r
 
 // FP32 estimate of count(tau) of unpinned stage r, clamped to [kmin, kmax]. Only a seed: the
 // threshold table confirms or corrects it (count_verify), so it never affects a result.
-template <int MAXS, class W>
-__device__ __forceinline__ int count_est(const W& w, const SweepSmem<MAXS>& sw, int r, float tf) {
+template <int MAXS, class W, class SW>
+__device__ __forceinline__ int count_est(const W& w, const SW& sw, int r, float tf) {
   const float* e = sw.est[r];
   const float q0 = e[2] * rcp_approx_f32(tf * e[0] - e[1]);
   const float q1 = e[5] * rcp_approx_f32(tf * e[3] - e[4]);
@@ -97,8 +97,8 @@ __device__ __forceinline__ double te_theta(const TEPair* row, int k) { return __
 // loads pk = {et(k), theta(k - 1)}, thk = theta(k): k is the count iff theta(k) <= tau <
 // theta(k - 1) (count(tau) = min{m : theta(m) <= tau}); otherwise the exact galloping table search
 // from k decides. Returns the count and et at it.
-template <int MAXS, class W>
-__device__ __forceinline__ int count_verify(const W& w, const SweepSmem<MAXS>& sw, int r,
+template <int MAXS, class W, class SW>
+__device__ __forceinline__ int count_verify(const W& w, const SW& sw, int r,
                                             double tau, int k, double2 pk, double thk, double& et) {
   if (thk <= tau && tau < pk.y) {
     et = pk.x;
@@ -118,9 +118,9 @@ struct CostScalars {  // the four job constants the cost needs (no parameter-str
 // one out-of-line copy shared by every call site.
 // gen = (g << 16) | m when tau = et_g(m) and tb.gex certifies count_g(tau) == m: every stage of
 // g's class then has count m and et == tau exactly (the breakpoint value itself).
-template <int MAXS, class W>
+template <int MAXS, class W, class SW>
 __device__ __noinline__ double cost_exact(const CostScalars cs, const W& w,
-                                          const SweepSmem<MAXS>& sw, int S, double tau, int gen) {
+                                          const SW& sw, int S, double tau, int gen) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   const int g = (gen >= 0) ? (gen >> 16) : -1, gm = gen & 0xffff;
   const float tf = (float)tau;
@@ -149,8 +149,8 @@ __device__ __noinline__ double cost_exact(const CostScalars cs, const W& w,
 }
 
 // exact cost of one candidate into the lane's tie buffer (one out-of-line copy for every site)
-template <int MAXS, class W>
-__device__ __noinline__ void eval_insert(const CostScalars cs, const W& w, const SweepSmem<MAXS>& sw,
+template <int MAXS, class W, class SW>
+__device__ __noinline__ void eval_insert(const CostScalars cs, const W& w, const SW& sw,
                                          int S, double tau, int gen, TieBuf& buf) {
   buf.insert(cost_exact<MAXS>(cs, w, sw, S, tau, gen), tau);
 }
@@ -197,8 +197,8 @@ __device__ __forceinline__ double cand_tau(const W& w, const SweepSmem<MAXS>& sw
 // candidate i of the restricted list: tau_lo, tau_hi, then per class leader sp the certified
 // breakpoints m in [alo, alo + an) (those inside the bound interval) and the uncertified ones
 // m in [blo, kmax]
-template <int MAXS, class W>
-__device__ __forceinline__ double cand_tau2(const W& w, const SweepSmem<MAXS>& sw, int i,
+template <int MAXS, class W, class SW>
+__device__ __forceinline__ double cand_tau2(const W& w, const SW& sw, int i,
                                             int& sp, double tau_lo, double tau_hi, int& gen) {
   gen = -1;
   if (i < 2) return (i == 0) ? tau_lo : tau_hi;
