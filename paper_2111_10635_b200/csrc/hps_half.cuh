@@ -384,6 +384,20 @@ __device__ __forceinline__ double seg_sumd(double v) {
   return v;
 }
 
+// WarpSmemL (hps_eval.cuh) without the final-phase fields (kres, tsum): the plan view of
+// prep_kernel_h, small enough that eight blocks of four warps (16 plans with their SweepSmem) fit
+// the 132 KB shared-memory configuration and leave the rest of the SM's 256 KB to the L1
+struct WarpSmemP {
+  const StageEntry* sp[16];
+  int32_t kmin[16];
+  int32_t kmax[16];
+  int32_t ent[16];
+  int32_t cls[16];
+  int32_t pre[17];
+  const TEPair* row[16];
+  __device__ __forceinline__ const StageEntry& stage(int r) const { return *sp[r]; }
+};
+
 // interval_cells (hps_sweep.cuh) for the plan of this half: segment lane j holds grid point j
 __device__ __noinline__ void interval_cells_half(double t, double L, double d, double thr, double& ta, double& tb) {
   const int sl = threadIdx.x & 15, base = threadIdx.x & 16;

@@ -1265,8 +1265,8 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, sl = lane & 15;
   const int v = warp * 2 + half;
-  WarpSmemL<16>& w = reinterpret_cast<WarpSmemL<16>*>(smem_raw)[v];
-  SweepSmem<16>& sw = reinterpret_cast<SweepSmem<16>*>(smem_raw + sizeof(WarpSmemL<16>) * WARPS * 2)[v];
+  WarpSmemP& w = reinterpret_cast<WarpSmemP*>(smem_raw)[v];
+  SweepSmem<16>& sw = reinterpret_cast<SweepSmem<16>*>(smem_raw + sizeof(WarpSmemP) * WARPS * 2)[v];
   const PlanState<16>* states = reinterpret_cast<const PlanState<16>*>(cont.states);
   const unsigned int n = *cont.count;
   const uint64_t gh = ((uint64_t)blockIdx.x * WARPS + warp) * 2 + half, nh = (uint64_t)gridDim.x * WARPS * 2;
@@ -1729,7 +1729,7 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   const size_t smemp = stage_offset<MAXS, WARPS>() + stage_bytes<MAXS, false>() * WARPS;
   CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemp));
   auto kph = prep_kernel_h<WARPS>;
-  const size_t smemph = (sizeof(WarpSmemL<16>) + sizeof(SweepSmem<16>)) * WARPS * 2;
+  const size_t smemph = (sizeof(WarpSmemP) + sizeof(SweepSmem<16>)) * WARPS * 2;
   if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(kph, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemph));
   auto k2 = candidate_kernel<MAXS, WARPS, ARGMIN>;
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
