@@ -960,6 +960,10 @@ struct HpsInstance {
   bool half_cand = true;    // L <= 16: two plans per warp in the candidate kernel (HPS_HALF_CAND=0: one)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
+  int pipe = 2;              // split-kernel chunk pipeline streams (HPS_PIPE=1: one stream)
+  uint64_t pipe_chunk = 1ull << 20;    // L <= 16 chunk size when pipelined (HPS_CHUNK overrides)
+  cudaStream_t aux = nullptr;          // the pipeline's second stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -1705,19 +1709,47 @@ int launch_stage(HpsInstance* in, const PlanSource& src, uint64_t p0, uint64_t p
   return HPS_OK;
 }
 
-// chunked K1a/K1b pair over plans [0, n); parts holds 2 * grid * WARPS partial keys
+// identity partial keys (a pipeline stream that received no chunk)
+__global__ void init_parts_kernel(KeyPart* parts, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    KeyPart kp;
+    kp.best.cost = __longlong_as_double(0x7ff0000000000000LL);
+    kp.best.hi = kp.best.lo = ~0ull;
+    kp.best.status = 0;
+    kp.evaluated = 0ull;
+    kp.feasible = 0ull;
+    kp.flags = 0u;
+    parts[i] = kp;
+  }
+}
+
+// streams of the chunk pipeline: 2 when the instance has its auxiliary stream (HPS_PIPE)
+int pipe_streams(const HpsInstance* in) { return (in->pipe > 1 && in->aux) ? 2 : 1; }
+
+// chunked K1a/K1b/K1c pipeline over plans [0, n); parts holds 2 * grid * WARPS partial keys per
+// pipeline stream. With two streams, chunk j runs on stream j % 2 with its own plan-state buffer
+// and partials, so one chunk's kernel tails overlap the other's kernels and a chunk's state
+// records (written by one kernel, read by the next) stay in L2 at small chunk sizes.
 template <int MAXS, int WARPS, bool ARGMIN>
 int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs& o, Pending pend,
               int feasible_only, KeyPart* parts, int grid, cudaStream_t st) {
-  const uint64_t base_chunk = in->chunk ? in->chunk : (MAXS <= 16 ? (4ull << 20) : (MAXS <= 32 ? (2ull << 20) : (1ull << 20)));
-  const uint64_t chunk = std::min<uint64_t>(n, base_chunk);
+  int np = pipe_streams(in);
+  const uint64_t def_chunk = (MAXS <= 16 ? (np > 1 ? in->pipe_chunk : (4ull << 20)) : (MAXS <= 32 ? (2ull << 20) : (1ull << 20)));
+  const uint64_t base_chunk = in->chunk ? in->chunk : def_chunk;
+  uint64_t chunk = std::min<uint64_t>(n, base_chunk);
+  if (np > 1) chunk = std::min<uint64_t>(chunk, (n + 1) / 2);   // >= 2 chunks when n >= 2
+  const uint64_t nchunks = (n + chunk - 1) / chunk;
+  const int used = (int)std::min<uint64_t>((uint64_t)np, nchunks);
   char* buf = nullptr;
   const size_t state_bytes = (sizeof(PlanState<MAXS>) * chunk + 255) / 256 * 256;
-  CUDA_TRY(cudaMallocAsync(&buf, state_bytes + sizeof(PrepState<MAXS>) * chunk + 256, st));
-  Cont cont{buf + 256, reinterpret_cast<unsigned int*>(buf), (unsigned int)chunk};
-  PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(buf + 256 + state_bytes);
-  KeyPart* parts_a = parts;
-  KeyPart* parts_b = parts ? parts + (size_t)grid * WARPS : nullptr;
+  const size_t slot_bytes = 256 + state_bytes + (sizeof(PrepState<MAXS>) * chunk + 255) / 256 * 256;
+  CUDA_TRY(cudaMallocAsync(&buf, slot_bytes * used, st));
+  const size_t nkp = (size_t)grid * WARPS;   // partials per kernel
+  if (ARGMIN && parts && used < np) {   // the second stream's partials are read by finish_argmin
+    HPS_COUNT_LAUNCH();
+    init_parts_kernel<<<8, 256, 0, st>>>(parts + 2 * nkp, (int)(2 * nkp));
+    CUDA_TRY(cudaGetLastError());
+  }
   const size_t smem3 = stage_offset<MAXS, WARPS>() + (stage_bytes<MAXS, true>() + sizeof(CandQueue)) * WARPS;
   const size_t smem1 = (sizeof(WarpSmemL<MAXS>) * WARPS + 15) / 16 * 16 + stage_bytes<MAXS, false>() * WARPS;
   auto kb = bisect_kernel<MAXS, WARPS>;
@@ -1738,38 +1770,53 @@ int run_split(HpsInstance* in, const PlanSource& src, uint64_t n, const Outputs&
   if (MAXS == 16) CUDA_TRY(cudaFuncSetAttribute(k2h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2h));
   if (MAXS == 16 && in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2h, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
   if (in->carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributePreferredSharedMemoryCarveout, in->carveout));
-  for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
-    const uint64_t c1 = std::min(n, c0 + chunk);
-    const int first = (c0 == 0);
-    CUDA_TRY(cudaMemsetAsync(cont.count, 0, sizeof(unsigned int), st));
+  if (used > 1) {   // fork: the auxiliary stream starts after everything queued on st so far
+    CUDA_TRY(cudaEventRecord(in->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(in->aux, in->ev_fork, 0));
+  }
+  for (uint64_t j = 0; j < nchunks; j++) {
+    const int sl = (int)(j % (uint64_t)used);
+    cudaStream_t s = sl ? in->aux : st;
+    const uint64_t c0 = j * chunk, c1 = std::min(n, c0 + chunk);
+    const int first = (j < (uint64_t)used);
+    char* sb = buf + slot_bytes * sl;
+    Cont cont{sb + 256, reinterpret_cast<unsigned int*>(sb), (unsigned int)chunk};
+    PrepState<MAXS>* prep = reinterpret_cast<PrepState<MAXS>*>(sb + 256 + state_bytes);
+    KeyPart* parts_a = parts ? parts + 2 * nkp * sl : nullptr;
+    KeyPart* parts_b = parts ? parts_a + nkp : nullptr;
+    CUDA_TRY(cudaMemsetAsync(cont.count, 0, sizeof(unsigned int), s));
     int rc;
-    if (src.mode == 0) rc = launch_stage<MAXS, WARPS, ARGMIN, 0>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
-    else if (src.mode == 1) rc = launch_stage<MAXS, WARPS, ARGMIN, 1>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
-    else if (src.mode == 3) rc = launch_stage<MAXS, WARPS, ARGMIN, 3>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
-    else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, st);
+    if (src.mode == 0) rc = launch_stage<MAXS, WARPS, ARGMIN, 0>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, s);
+    else if (src.mode == 1) rc = launch_stage<MAXS, WARPS, ARGMIN, 1>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, s);
+    else if (src.mode == 3) rc = launch_stage<MAXS, WARPS, ARGMIN, 3>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, s);
+    else rc = launch_stage<MAXS, WARPS, ARGMIN, 2>(in, src, c0, c1, o, pend, cont, feasible_only, parts_a, first, grid, s);
     if (rc) return rc;
     HPS_COUNT_LAUNCH();
     if (MAXS == 16 && in->half_bisect) {   // two plans per warp (hps_half.cuh)
-      kbh<<<grid, WARPS * 32, smemh, st>>>(in->c, in->tb, cont, pend);
+      kbh<<<grid, WARPS * 32, smemh, s>>>(in->c, in->tb, cont, pend);
     } else {
-      kb<<<grid, WARPS * 32, smem1, st>>>(in->c, in->tb, cont, pend);
+      kb<<<grid, WARPS * 32, smem1, s>>>(in->c, in->tb, cont, pend);
     }
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
     if (MAXS == 16 && in->half_prep) {   // two plans per warp (hps_half.cuh)
-      kph<<<grid, WARPS * 32, smemph, st>>>(in->c, in->tb, cont, reinterpret_cast<PrepState<16>*>(prep));
+      kph<<<grid, WARPS * 32, smemph, s>>>(in->c, in->tb, cont, reinterpret_cast<PrepState<16>*>(prep));
     } else {
-      kp<<<grid, WARPS * 32, smemp, st>>>(in->c, in->tb, cont, prep);
+      kp<<<grid, WARPS * 32, smemp, s>>>(in->c, in->tb, cont, prep);
     }
     CUDA_TRY(cudaGetLastError());
     HPS_COUNT_LAUNCH();
     if (MAXS == 16 && in->half_cand) {   // two plans per warp (hps_half.cuh)
-      k2h<<<grid, WARPS * 32, smem2h, st>>>(in->c, in->tb, cont, reinterpret_cast<const PrepState<16>*>(prep), o,
-                                            feasible_only, parts_b, first);
+      k2h<<<grid, WARPS * 32, smem2h, s>>>(in->c, in->tb, cont, reinterpret_cast<const PrepState<16>*>(prep), o,
+                                           feasible_only, parts_b, first);
     } else {
-      k2<<<grid, WARPS * 32, smem3, st>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
+      k2<<<grid, WARPS * 32, smem3, s>>>(in->c, in->tb, cont, prep, o, feasible_only, parts_b, first);
     }
     CUDA_TRY(cudaGetLastError());
+  }
+  if (used > 1) {   // join
+    CUDA_TRY(cudaEventRecord(in->ev_join, in->aux));
+    CUDA_TRY(cudaStreamWaitEvent(st, in->ev_join, 0));
   }
   CUDA_TRY(cudaFreeAsync(buf, st));
   return HPS_OK;
@@ -1871,7 +1918,7 @@ int argmin_common(HpsInstance* in, PlanSource& src, uint64_t n, int feasible_onl
   const uint64_t nsc = (n + sc - 1) / sc;
   const uint64_t n0 = std::min(n, sc);
   const int grid = grid_for(in, n0);   // one grid for every chunk: every warp writes its partial
-  const int nparts = grid * warps_per_block(in) * (in->fast ? 2 : 1);
+  const int nparts = grid * warps_per_block(in) * (in->fast ? 2 * pipe_streams(in) : 1);
   int nslow = 0;
   if (int rc = slow_grid(in, nslow)) return rc;
   const unsigned cap = (unsigned)n0;
@@ -1972,6 +2019,12 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   if (const char* e = getenv("HPS_HALF_CAND")) in->half_cand = atoi(e) != 0;
   if (const char* e = getenv("HPS_CHUNK")) in->chunk = (uint64_t)std::max(1024ll, atoll(e));
   if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
+  if (const char* e = getenv("HPS_PIPE")) in->pipe = std::max(1, std::min(2, atoi(e)));
+  if (in->pipe > 1) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&in->aux, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&in->ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&in->ev_join, cudaEventDisableTiming));
+  }
   {  // keep stream-ordered scratch (slow-path buffers, argmin partials) mapped between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -2082,6 +2135,9 @@ int hps_instance_destroy(HpsInstance* in) {
   cudaFree(in->d_te);
   cudaFree(in->d_cls);
   cudaFree(in->d_gex);
+  if (in->aux) cudaStreamDestroy(in->aux);
+  if (in->ev_fork) cudaEventDestroy(in->ev_fork);
+  if (in->ev_join) cudaEventDestroy(in->ev_join);
   delete in;
   return HPS_OK;
 }
