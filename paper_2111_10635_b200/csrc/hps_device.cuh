@@ -21,7 +21,7 @@ typedef unsigned __int128 u128;
 enum {
   ST_PLANS, ST_CHUNKS, ST_CHUNKS_EVAL, ST_CANDS, ST_PROBES_EXACT, ST_PROBES_CLOSED, ST_CERT,
   ST_CERT_FAIL, ST_TAB, ST_PENDING, ST_STAGES, ST_UNPINNED, ST_NCAND, ST_PLANS_FAST,
-  ST_CYC_A, ST_CYC_B, ST_CYC_C, ST_CYC_P1, ST_CYC_P2, ST_N2, ST_UNCERT, ST_NSTAT
+  ST_CYC_A, ST_CYC_B, ST_CYC_C, ST_CYC_P1, ST_CYC_P2, ST_N2, ST_UNCERT, ST_IDEAL, ST_IDEAL2, ST_NEAR, ST_NSTAT
 };
 #ifdef HPS_STATS
 __device__ unsigned long long g_stats[24];

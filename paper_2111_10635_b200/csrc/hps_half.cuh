@@ -428,7 +428,8 @@ __device__ __noinline__ void interval_cells_half(double t, double L, double d, d
 // and grid point sl; the warm start evaluates the same 32 candidates in two rounds of 16.
 template <int MAXS, class W>
 __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb, const W& w, SweepSmem<MAXS>& sw,
-                                 int S, double tau_lo, double tau_hi, int n_cand, TieBuf& buf) {
+                                 int S, double tau_lo, double tau_hi, int n_cand, TieBuf& buf,
+                                 int& kbv, double& tb_out, float& pb_out) {
   const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
   const unsigned am = seg_mask();
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
@@ -535,13 +536,19 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
       interval_cells_half(t1, L1, d1, thr, ta, tbh);
     }
   }
+  // count of every stage at tau_b: a candidate tau <= tau_b has count_r(tau) >= count_r(tau_b)
+  // for every r (counts are non-increasing), the candidate filter's base (cand_main_half)
+  kbv = mine ? sw.kmi[r] : 0;
+  if (mine && !pinned && ta <= tbh) kbv = count_seeded(w.stage(r), w.row[r], tbh, sw.kmi[r], sw.kma[r]);
+  pb_out = seg_sumf(mine ? sw.fpr[r] * (float)kbv : 0.0f);
+  tb_out = (ta <= tbh) ? tbh : -inf;
   if (mine) {
     if (w.pre[r + 1] > w.pre[r]) {  // class leader with breakpoints
       const int lo = sw.kmi[r], hi = sw.kma[r];
       int alo = 0, an = 0;
       const int chi = min(hi, sw.gex[r]);
       if (ta <= tbh && chi >= lo) {
-        const int ma = count_seeded(w.stage(r), w.row[r], tbh, lo, hi);
+        const int ma = kbv;
         const int mb = count_seeded(w.stage(r), w.row[r], ta, lo, hi);
         alo = max(ma, lo);
         an = max(0, min(mb, chi) - alo + 1);
@@ -577,8 +584,14 @@ struct CandView {
   int32_t pre2[17];
   int32_t top;
   int16_t alo[16], an[16], blo[16];
+  int16_t kb[16];      // count at tau_b (cand_prep_half)
   int8_t lead[16], type[16];
   uint32_t tsum[kMaxT];
+  double tb;           // tau_b: right end of the restricted interval (-inf: none)
+  float pb;            // FP32 sum of pr * count at tau_b
+  float p0f;           // FP32 sum of pr * count over the pinned stages
+  int32_t nu;          // unpinned stages, in stage order:
+  int8_t ulist[16];
 };
 
 // count_lb32 (hps_sweep.cuh) from the count_est seeds: they hold the same FP32 side constants, with
@@ -597,6 +610,21 @@ __device__ __forceinline__ int count_lb32_est(const float* e, float tau) {
     lo = fmaxf(lo, (frac * rh) * (1.0f - ee));
   }
   return (int)ceilf(lo);
+}
+
+// FP32 lower bound of P(tau) = sum_r pr_r count_r(tau) at a certified breakpoint tau = et_g(m) in
+// [tau_lo, tau_hi]: g's class has count m; every other unpinned stage's count is >= its count at
+// tau_hi (at tau_b when tau <= tau_b) and >= count_lb32_est; pinned stages are exact (p0f).
+__device__ __forceinline__ float filter_P(const CandView& v, int g, int m, double tau, float tf) {
+  const bool inb = tau <= v.tb;
+  float P = v.p0f;
+  for (int j = 0; j < v.nu; j++) {
+    const int r = v.ulist[j];
+    int k = m;
+    if (v.lead[r] != g) k = max(inb ? (int)v.kb[r] : v.kmi[r], count_lb32_est(v.est[r], tf));
+    P += v.fpr[r] * (float)k;
+  }
+  return P;
 }
 
 // overflow_pass (hps_sweep.cuh) for the plan of this half: candidates strided over 16 lanes
@@ -645,8 +673,14 @@ __device__ double cand_main_half(const InstanceConsts& c, CandView& v, CandQueue
   }
 #endif
   const float fC = (float)(c.work / c.batch);
-  const float pl0 = seg_sumf((sl < S) ? v.fpr[sl] * (float)v.kmi[sl] : 0.0f);  // sum of pr count(tau_hi)
-  const int top = v.top;
+  {  // unpinned stages in order, and the pinned stages' part of filter_P
+    const bool unp = sl < S && v.kma[sl] != v.kmi[sl];
+    const unsigned um = seg_ballot(unp);
+    if (unp) v.ulist[__popc(um & ((1u << sl) - 1u))] = (int8_t)sl;
+    const float p0f = seg_sumf((sl < S && !unp) ? v.fpr[sl] * (float)v.kmi[sl] : 0.0f);
+    if (sl == 0) { v.nu = __popc(um); v.p0f = p0f; }
+    __syncwarp(am);
+  }
   double* qt = cq.q + 2 * base;      // this half's 32 queue slots
   int32_t* qg = cq.qg + 2 * base;
   int sp = 0, qn = 0;
@@ -660,14 +694,9 @@ __device__ double cand_main_half(const InstanceConsts& c, CandView& v, CandQueue
     if (i < n2) {
       tau = cand_tau2<16>(v, v, i, sp, tau_lo, tau_hi, gen);
       keep = tau >= tau_lo && tau <= tau_hi;
-      if (keep && gen >= 0) {
-        const int g = gen >> 16, m = gen & 0xffff;
+      if (keep && gen >= 0) {   // cost >= C tau P(tau) (E >= tau at a certified breakpoint)
         const float tf = (float)tau;
-        float P = pl0 + v.fpr[g] * (float)(m - v.kmi[g]);
-        if (top >= 0 && top != g) {
-          const int d = count_lb32_est(v.est[top], tf) - v.kmi[top];
-          if (d > 0) P += v.fpr[top] * (float)d;
-        }
+        const float P = filter_P(v, gen >> 16, gen & 0xffff, tau, tf);
         keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > ub + 1e-15);
       }
     }
@@ -690,6 +719,37 @@ __device__ double cand_main_half(const InstanceConsts& c, CandView& v, CandQueue
     eval_insert<16>(cs, v, v, S, qt[sl], qg[sl], buf);
   }
   const double mf = seg_min(buf.mn);
+#ifdef HPS_STATS
+  {  // analysis only: survivors of the same filter with the final minimum as ub (IDEAL), and with
+     // exact counts of every stage except E >= tau (IDEAL2: the best any count bound can do)
+    int spx = 0;
+    for (int jr = 0; jr < rounds; jr++) {
+      const int i = jr * 16 + sl;
+      if (i >= n2) continue;
+      int gen;
+      const double tau = cand_tau2<16>(v, v, i, spx, tau_lo, tau_hi, gen);
+      if (!(tau >= tau_lo && tau <= tau_hi)) continue;
+      bool keep = true, keep2 = true;
+      if (gen >= 0) {
+        const float tf = (float)tau;
+        const float P = filter_P(v, gen >> 16, gen & 0xffff, tau, tf);
+        keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > mf + 1e-15);
+        // exact P at tau
+        double Px = 0.0;
+        for (int r = 0; r < S; r++) {
+          int k;
+          if (v.kma[r] == v.kmi[r]) k = v.kmi[r];
+          else { double et; const int k0 = count_est<16>(v, v, r, tf); k = count_verify<16>(v, v, r, tau, k0, te_pair(v.row[r], k0), te_theta(v.row[r], k0), et); }
+          Px += v.pr[r] * (double)k;
+        }
+        keep2 = !((c.work / c.batch) * tau * Px * (1.0 - 1e-12) > mf + 1e-15);
+      }
+      if (keep) HPS_STAT(ST_IDEAL, 1);
+      if (keep2) HPS_STAT(ST_IDEAL2, 1);
+      if (cost_exact<16>(cs, v, v, S, tau, gen) <= mf * (1.0 + 1e-3)) HPS_STAT(ST_NEAR, 1);
+    }
+  }
+#endif
   if (!(mf < inf)) return __longlong_as_double(0x7ff8000000000000LL);
   const double lim = mf + 1e-15;
   double bt;

@@ -1011,9 +1011,12 @@ struct Cont {
 template <int MAXS>
 struct __align__(16) PrepState {
   double ub;
+  double tb;      // right end of the restricted interval (half-warp kernels; -inf: none)
   int32_t top;
+  float pb;       // FP32 sum of pr * count at tb (half-warp kernels)
   int8_t dom[MAXS], lead[MAXS];
   int16_t alo[MAXS], an[MAXS], blo[MAXS];
+  int16_t kb[MAXS];   // count at tb (half-warp kernels)
 };
 
 // double-buffered per-warp staging of the next plan's state records (bulk copies, hps_tma.cuh)
@@ -1295,9 +1298,13 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
       __syncwarp(seg_mask());
       TieBuf buf;
       buf.init();
-      const double ub = cand_prep_half<16>(c, tb, w, sw, S, ps.tau_lo, ps.tau_hi, ps.n_cand, buf);
+      int kbv;
+      double tbv;
+      float pbv;
+      const double ub = cand_prep_half<16>(c, tb, w, sw, S, ps.tau_lo, ps.tau_hi, ps.n_cand, buf, kbv, tbv, pbv);
       PrepState<16>& out = prep[q];
       if (sl < S) {
+        out.kb[sl] = (int16_t)kbv;
         out.dom[sl] = (int8_t)sw.dom[sl];
         out.lead[sl] = sw.lead[sl];
         out.alo[sl] = (int16_t)sw.alo[sl];
@@ -1306,6 +1313,8 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
       }
       if (sl == 0) {
         out.ub = ub;
+        out.tb = tbv;
+        out.pb = pbv;
         out.top = sw.top[0];
       }
     }
@@ -1367,8 +1376,13 @@ candidate_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, con
       v.alo[sl] = pp.alo[sl];
       v.an[sl] = pp.an[sl];
       v.blo[sl] = pp.blo[sl];
+      v.kb[sl] = pp.kb[sl];
     }
-    if (sl == 0) v.top = pp.top;
+    if (sl == 0) {
+      v.top = pp.top;
+      v.tb = pp.tb;
+      v.pb = pp.pb;
+    }
     __syncwarp(am);
     PlanOut r;
     r.ps = 0;

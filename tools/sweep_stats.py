@@ -7,9 +7,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-NAMES = ["plans", "ideal_survivors", "gen_certified", "cands_eval", "probes_exact", "probes_closed", "cert",
-         "cert_fail", "tab", "pending", "stages", "bisect_fallback", "ncand", "plans_fast", "cyc_stages_bisect", "cyc_candidates",
-         "cyc_final", "cyc_pass1", "cyc_pass2", "n2_restricted", "n2_uncertified"]
+NAMES = ["plans", "chunks", "chunks_eval", "cands_eval", "probes_exact", "probes_closed", "cert", "cert_fail",
+         "tab", "pending", "stages", "unpinned", "ncand", "plans_fast", "cyc_a", "cyc_b", "cyc_c", "cyc_p1",
+         "cyc_p2", "n2_restricted", "n2_uncertified", "ideal_survivors", "ideal2_survivors", "near_1e-3"]
 
 
 def main():
@@ -36,7 +36,7 @@ def main():
     st = dict(zip(NAMES, list(buf)[:len(NAMES)]))
     print(key)
     print(st)
-    pf = max(1, st["plans_fast"])
+    pf = max(1, int(os.environ.get("STATS_PLANS", "0")) or st["plans_fast"] or 1)
     print({k: round(v / pf, 2) for k, v in st.items()})
 
 
