@@ -429,7 +429,7 @@ __device__ __noinline__ void interval_cells_half(double t, double L, double d, d
 template <int MAXS, class W>
 __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb, const W& w, SweepSmem<MAXS>& sw,
                                  int S, double tau_lo, double tau_hi, int n_cand, TieBuf& buf,
-                                 int& kbv, double& tb_out, float& pb_out) {
+                                 int& kbv, double& tb_out) {
   const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
   const unsigned am = seg_mask();
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
@@ -540,7 +540,6 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
   // for every r (counts are non-increasing), the candidate filter's base (cand_main_half)
   kbv = mine ? sw.kmi[r] : 0;
   if (mine && !pinned && ta <= tbh) kbv = count_seeded(w.stage(r), w.row[r], tbh, sw.kmi[r], sw.kma[r]);
-  pb_out = seg_sumf(mine ? sw.fpr[r] * (float)kbv : 0.0f);
   tb_out = (ta <= tbh) ? tbh : -inf;
   if (mine) {
     if (w.pre[r + 1] > w.pre[r]) {  // class leader with breakpoints
@@ -574,24 +573,28 @@ namespace hps {
 // the final counts read, packed so that eight blocks of four warps (16 plans) fit the 132 KB
 // shared-memory configuration and leave the rest of the SM's 256 KB to the L1 (table loads).
 // It serves as both the plan view (row) and the sweep constants of the shared helpers.
-struct CandView {
+struct __align__(16) CandView {
   const TEPair* row[16];
   double pr[16];       // price per second of stage r's type
   double etp[16];      // et at the pinned count (kmin == kmax)
-  float est[16][6];    // count_est seeds; a side off per side_dominance is {0, -1, 0}
-  float fpr[16];
+  // per stage, two 16-byte records read by one LDS.128 each: {rb, 1 - frac, frac} of side 0 (oct)
+  // and side 1 (odt) = the count_est seeds (a side off per side_dominance is {0, -1, 0}), then
+  // pr as FP32 and the counts at tau_hi (low 16 bits) and tau_b (high 16 bits)
+  float4 fe[16][2];
   int32_t kmi[16], kma[16];
   int32_t pre2[17];
-  int32_t top;
   int16_t alo[16], an[16], blo[16];
-  int16_t kb[16];      // count at tau_b (cand_prep_half)
   int8_t lead[16], type[16];
   uint32_t tsum[kMaxT];
   double tb;           // tau_b: right end of the restricted interval (-inf: none)
-  float pb;            // FP32 sum of pr * count at tau_b
   float p0f;           // FP32 sum of pr * count over the pinned stages
-  int32_t nu;          // unpinned stages, in stage order:
-  int8_t ulist[16];
+  uint32_t umask;      // unpinned stages (bit r)
+  __device__ __forceinline__ float est_at(int r, int i) const {
+    const float4& q = fe[r][i / 3];
+    const int j = i % 3;
+    return j == 0 ? q.x : (j == 1 ? q.y : q.z);
+  }
+  __device__ __forceinline__ float fpr(int r) const { return fe[r][0].w; }
 };
 
 // count_lb32 (hps_sweep.cuh) from the count_est seeds: they hold the same FP32 side constants, with
@@ -616,13 +619,26 @@ __device__ __forceinline__ int count_lb32_est(const float* e, float tau) {
 // [tau_lo, tau_hi]: g's class has count m; every other unpinned stage's count is >= its count at
 // tau_hi (at tau_b when tau <= tau_b) and >= count_lb32_est; pinned stages are exact (p0f).
 __device__ __forceinline__ float filter_P(const CandView& v, int g, int m, double tau, float tf) {
-  const bool inb = tau <= v.tb;
+  const int sh = (tau <= v.tb) ? 16 : 0;   // floor: count at tau_b, else at tau_hi
   float P = v.p0f;
-  for (int j = 0; j < v.nu; j++) {
-    const int r = v.ulist[j];
-    int k = m;
-    if (v.lead[r] != g) k = max(inb ? (int)v.kb[r] : v.kmi[r], count_lb32_est(v.est[r], tf));
-    P += v.fpr[r] * (float)k;
+  for (unsigned um = v.umask; um; um &= um - 1) {
+    const int r = __ffs(um) - 1;
+    const float4 a = v.fe[r][0], b = v.fe[r][1];
+    float lo = 1.0f;   // count_lb32_est over the two sides
+#pragma unroll
+    for (int side = 0; side < 2; side++) {
+      const float rb = side ? b.x : a.x, omf = side ? b.y : a.y, frac = side ? b.z : a.z;
+      const float B = tf * rb;
+      const float h = B - omf;
+      if (rb != 0.0f && h > 1e-3f * B) {
+        const float rh = rcp_approx_f32(h);
+        const float ee = 4e-7f * (B * rh + 2.0f) + 1e-6f;
+        lo = fmaxf(lo, (frac * rh) * (1.0f - ee));
+      }
+    }
+    const int fl = (int)((__float_as_uint(b.w) >> sh) & 0xffffu);
+    const int k = (v.lead[r] == g) ? m : max(fl, (int)ceilf(lo));
+    P += a.w * (float)k;
   }
   return P;
 }
@@ -676,9 +692,8 @@ __device__ double cand_main_half(const InstanceConsts& c, CandView& v, CandQueue
   {  // unpinned stages in order, and the pinned stages' part of filter_P
     const bool unp = sl < S && v.kma[sl] != v.kmi[sl];
     const unsigned um = seg_ballot(unp);
-    if (unp) v.ulist[__popc(um & ((1u << sl) - 1u))] = (int8_t)sl;
-    const float p0f = seg_sumf((sl < S && !unp) ? v.fpr[sl] * (float)v.kmi[sl] : 0.0f);
-    if (sl == 0) { v.nu = __popc(um); v.p0f = p0f; }
+    const float p0f = seg_sumf((sl < S && !unp) ? v.fpr(sl) * (float)v.kmi[sl] : 0.0f);
+    if (sl == 0) { v.umask = um; v.p0f = p0f; }
     __syncwarp(am);
   }
   double* qt = cq.q + 2 * base;      // this half's 32 queue slots

@@ -1013,7 +1013,6 @@ struct __align__(16) PrepState {
   double ub;
   double tb;      // right end of the restricted interval (half-warp kernels; -inf: none)
   int32_t top;
-  float pb;       // FP32 sum of pr * count at tb (half-warp kernels)
   int8_t dom[MAXS], lead[MAXS];
   int16_t alo[MAXS], an[MAXS], blo[MAXS];
   int16_t kb[MAXS];   // count at tb (half-warp kernels)
@@ -1300,8 +1299,7 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
       buf.init();
       int kbv;
       double tbv;
-      float pbv;
-      const double ub = cand_prep_half<16>(c, tb, w, sw, S, ps.tau_lo, ps.tau_hi, ps.n_cand, buf, kbv, tbv, pbv);
+      const double ub = cand_prep_half<16>(c, tb, w, sw, S, ps.tau_lo, ps.tau_hi, ps.n_cand, buf, kbv, tbv);
       PrepState<16>& out = prep[q];
       if (sl < S) {
         out.kb[sl] = (int16_t)kbv;
@@ -1314,7 +1312,6 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
       if (sl == 0) {
         out.ub = ub;
         out.tb = tbv;
-        out.pb = pbv;
         out.top = sw.top[0];
       }
     }
@@ -1358,31 +1355,31 @@ candidate_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, con
       v.row[sl] = row;
       v.type[sl] = (int8_t)type;
       v.pr[sl] = c.price_s[type];
-      v.fpr[sl] = (float)c.price_s[type];
+
       v.kmi[sl] = lo;
       v.kma[sl] = hi;
       v.etp[sl] = (lo == hi) ? __ldg(&HPS_TE(row, lo - 1).et) : 0.0;
       const int dom = pp.dom[sl];
+      float4 fr[2];
 #pragma unroll
       for (int side = 0; side < 2; side++) {   // est_setup (hps_sweep.cuh)
         const float rb = __ldg(side ? &st->f_rbd : &st->f_rbo);
         const float frac = __ldg(side ? &st->f_beta : &st->f_alpha);
         const bool on = (dom != 2 - side) && rb != 0.0f && frac != 0.0f;
-        v.est[sl][3 * side + 0] = on ? rb : 0.0f;
-        v.est[sl][3 * side + 1] = on ? __ldg(side ? &st->f_omb : &st->f_oma) : -1.0f;
-        v.est[sl][3 * side + 2] = on ? frac : 0.0f;
+        fr[side].x = on ? rb : 0.0f;
+        fr[side].y = on ? __ldg(side ? &st->f_omb : &st->f_oma) : -1.0f;
+        fr[side].z = on ? frac : 0.0f;
       }
+      fr[0].w = (float)c.price_s[type];
+      fr[1].w = __uint_as_float((uint32_t)(lo & 0xffff) | ((uint32_t)(pp.kb[sl] & 0xffff) << 16));
+      v.fe[sl][0] = fr[0];
+      v.fe[sl][1] = fr[1];
       v.lead[sl] = pp.lead[sl];
       v.alo[sl] = pp.alo[sl];
       v.an[sl] = pp.an[sl];
       v.blo[sl] = pp.blo[sl];
-      v.kb[sl] = pp.kb[sl];
     }
-    if (sl == 0) {
-      v.top = pp.top;
-      v.tb = pp.tb;
-      v.pb = pp.pb;
-    }
+    if (sl == 0) v.tb = pp.tb;
     __syncwarp(am);
     PlanOut r;
     r.ps = 0;

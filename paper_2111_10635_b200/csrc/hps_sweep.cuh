@@ -53,6 +53,7 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   double p0;         // sum over pinned stages of pr * count (the bound's linear part)
   int32_t nu;        // unpinned stages, in stage order:
   int8_t ulist[MAXS];
+  __device__ __forceinline__ float est_at(int r, int i) const { return est[r][i]; }
 };
 
 // FP32 estimate of count(tau) of unpinned stage r, clamped to [kmin, kmax]. Only a seed: the
@@ -78,9 +79,8 @@ __device__ __forceinline__ void est_setup(const W& w, SweepSmem<MAXS>& sw, int r
 // threshold table confirms or corrects it (count_verify), so it never affects a result.
 template <int MAXS, class W, class SW>
 __device__ __forceinline__ int count_est(const W& w, const SW& sw, int r, float tf) {
-  const float* e = sw.est[r];
-  const float q0 = e[2] * rcp_approx_f32(tf * e[0] - e[1]);
-  const float q1 = e[5] * rcp_approx_f32(tf * e[3] - e[4]);
+  const float q0 = sw.est_at(r, 2) * rcp_approx_f32(tf * sw.est_at(r, 0) - sw.est_at(r, 1));
+  const float q1 = sw.est_at(r, 5) * rcp_approx_f32(tf * sw.est_at(r, 3) - sw.est_at(r, 4));
   const float q = fmaxf(1.0f, fmaxf(q0, q1));   // (NaN operands are ignored)
   const int lo = sw.kmi[r], hi = sw.kma[r];
   const int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
