@@ -68,6 +68,18 @@ struct PlanOut {
   int ps;
 };
 
+// `steps` of the reference's quota bisection (ls/provisioner.py:430-436) once quota_ok(mid) is known to
+// be (mid >= tstar). A step whose midpoint equals a or b is the last that can change anything (the
+// next midpoints repeat it, or a == b), so the loop stops there with the same (a, b) as all steps.
+__device__ __forceinline__ void halvings(double& a, double& b, double tstar, int steps) {
+  for (int it = 0; it < steps; it++) {
+    const double mid = (a + b) / 2.0;
+    const bool last = (mid == a) || (mid == b);
+    if (mid >= tstar) b = mid; else a = mid;
+    if (last) break;
+  }
+}
+
 struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min + 1e-15
   double c[kTieBuf], t[kTieBuf];
   int n;
@@ -341,10 +353,7 @@ __device__ __forceinline__ double bisect_fast(const InstanceConsts& c, const Dev
       lo_bound = x;
     }
     if (lane == 0) HPS_STAT(ST_PROBES_CLOSED, 60 - it);
-    for (; it < 60; it++) {
-      const double mid = (a + b) / 2.0;
-      if (mid >= tstar) b = mid; else a = mid;
-    }
+    halvings(a, b, tstar, 60 - it);
     for (int slot = 0; slot < 2; slot++)
       if (ub[slot] != lb[slot] && b < thr_lb[slot]) lb[slot] = ub[slot];
   }
@@ -538,10 +547,7 @@ __device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W
     tstar = fmax(tstar, tt);
   }
   if (lane == 0) HPS_STAT(ST_PROBES_CLOSED, 60);
-  for (int it = 0; it < 60; it++) {
-    const double mid = (a + b) / 2.0;
-    if (mid >= tstar) b = mid; else a = mid;
-  }
+  halvings(a, b, tstar, 60);
 #pragma unroll
   for (int slot = 0; slot < 2; slot++)
     kb_out[slot] = (ty[slot] >= 0) ? count_seeded(w.stage(lane + 32 * slot), row[slot], b, kb[slot], (int)c.quota[ty[slot]])

@@ -143,10 +143,7 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
     }
     tstar = fmax(tstar, tt);
   }
-  for (int it = 0; it < 60; it++) {   // the reference's halvings (ls/provisioner.py:430-436)
-    const double mid = (a + b) / 2.0;
-    if (mid >= tstar) b = mid; else a = mid;
-  }
+  halvings(a, b, tstar, 60);   // the reference's halvings (ls/provisioner.py:430-436)
   kb_out = (ty >= 0) ? count_seeded(w.stage(sl), row, b, kb, (int)c.quota[ty]) : kb;
   return b;
 }
@@ -596,24 +593,6 @@ struct __align__(16) CandView {
   }
   __device__ __forceinline__ float fpr(int r) const { return fe[r][0].w; }
 };
-
-// count_lb32 (hps_sweep.cuh) from the count_est seeds: they hold the same FP32 side constants, with
-// the sides count_lb32 skips (dominated, rb == 0 or frac == 0) set to rb = 0
-__device__ __forceinline__ int count_lb32_est(const float* e, float tau) {
-  float lo = 1.0f;
-#pragma unroll
-  for (int side = 0; side < 2; side++) {
-    const float rb = e[3 * side], omf = e[3 * side + 1], frac = e[3 * side + 2];
-    if (rb == 0.0f) continue;
-    const float B = tau * rb;
-    const float h = B - omf;
-    if (!(h > 1e-3f * B)) continue;
-    const float rh = rcp_approx_f32(h);
-    const float ee = 4e-7f * (B * rh + 2.0f) + 1e-6f;
-    lo = fmaxf(lo, (frac * rh) * (1.0f - ee));
-  }
-  return (int)ceilf(lo);
-}
 
 // FP32 lower bound of P(tau) = sum_r pr_r count_r(tau) at a certified breakpoint tau = et_g(m) in
 // [tau_lo, tau_hi]: g's class has count m; every other unpinned stage's count is >= its count at

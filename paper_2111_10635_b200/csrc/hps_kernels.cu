@@ -1566,6 +1566,7 @@ prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<
     const double ub = cand_prep<MAXS>(c, tb, w, sw, S, ps.tau_lo, ps.tau_hi, ps.n_cand, buf);
     PrepState<MAXS>& out = prep[q];
     for (int s = lane; s < S; s += 32) {
+      out.kb[s] = sw.kb[s];
       out.dom[s] = (int8_t)sw.dom[s];
       out.lead[s] = sw.lead[s];
       out.alo[s] = (int16_t)sw.alo[s];
@@ -1574,6 +1575,7 @@ prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<
     }
     if (lane == 0) {
       out.ub = ub;
+      out.tb = sw.tb;
       out.top = sw.top[0];
     }
     __syncwarp();
@@ -1631,8 +1633,12 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
       sw.alo[r] = pp.alo[r];
       sw.an[r] = pp.an[r];
       sw.blo[r] = pp.blo[r];
+      sw.kb[r] = pp.kb[r];
     }
-    if (lane == 0) sw.top[0] = pp.top;
+    if (lane == 0) {
+      sw.top[0] = pp.top;
+      sw.tb = pp.tb;
+    }
     __syncwarp();
     PlanOut r;
     r.ps = 0;

@@ -53,6 +53,9 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   double p0;         // sum over pinned stages of pr * count (the bound's linear part)
   int32_t nu;        // unpinned stages, in stage order:
   int8_t ulist[MAXS];
+  int16_t kb[MAXS];  // count at tb (cand_prep): the candidate filter's floor for tau <= tb
+  double tb;         // right end of the restricted interval (-inf: none)
+  float p0f;         // pinned stages' sum of pr * count in FP32 (cand_main)
   __device__ __forceinline__ float est_at(int r, int i) const { return est[r][i]; }
 };
 
@@ -176,6 +179,24 @@ __device__ __forceinline__ int count_lb32(const StageEntry& s, float tau, int do
     const float rh = rcp_approx_f32(h);
     const float e = 4e-7f * (B * rh + 2.0f) + 1e-6f;
     lo = fmaxf(lo, (frac * rh) * (1.0f - e));
+  }
+  return (int)ceilf(lo);
+}
+
+// count_lb32 from the count_est seed constants (est_setup): they hold the same FP32 side constants,
+// with the sides count_lb32 skips (dominated, rb == 0 or frac == 0) set to rb = 0
+__device__ __forceinline__ int count_lb32_est(const float* e, float tau) {
+  float lo = 1.0f;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const float rb = e[3 * side], omf = e[3 * side + 1], frac = e[3 * side + 2];
+    if (rb == 0.0f) continue;
+    const float B = tau * rb;
+    const float h = B - omf;
+    if (!(h > 1e-3f * B)) continue;
+    const float rh = rcp_approx_f32(h);
+    const float ee = 4e-7f * (B * rh + 2.0f) + 1e-6f;
+    lo = fmaxf(lo, (frac * rh) * (1.0f - ee));
   }
   return (int)ceilf(lo);
 }
@@ -458,15 +479,23 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
     }
   }
   {
+    if (lane == 0) sw.tb = (ta <= tbh) ? tbh : -inf;
 #pragma unroll
     for (int slot = 0; slot < 2; slot++) {
       const int r = lane + 32 * slot;
+      // count at tau_b of every stage: a candidate tau <= tau_b has count_r(tau) >= it
+      int kbv = 0;
+      if (r < S) {
+        kbv = sw.kmi[r];
+        if (sw.kma[r] != sw.kmi[r] && ta <= tbh) kbv = count_seeded(w.stage(r), w.row[r], tbh, sw.kmi[r], sw.kma[r]);
+        sw.kb[r] = (int16_t)kbv;
+      }
       if (r < S && w.pre[r + 1] > w.pre[r]) {  // class leader with breakpoints
         const int lo = sw.kmi[r], hi = sw.kma[r];
         int alo = 0, an = 0;
         const int chi = min(hi, sw.gex[r]);   // certified part [lo, chi]
         if (ta <= tbh && chi >= lo) {
-          const int ma = count_seeded(w.stage(r), w.row[r], tbh, lo, hi);  // smallest certified m
+          const int ma = kbv;  // smallest certified m
           const int mb = count_seeded(w.stage(r), w.row[r], ta, lo, hi);   // largest certified m
           alo = max(ma, lo);
           an = max(0, min(mb, chi) - alo + 1);
@@ -526,13 +555,22 @@ __device__ double cand_main(const InstanceConsts& c, const W& w, SweepSmem<MAXS>
   }
 #endif
   const float fC = (float)C;
-  float pl0 = 0.0f;  // sum of pr count(tau_hi)
-#pragma unroll 1
-  for (int r = lane; r < S; r += 32) pl0 += sw.fpr[r] * (float)sw.kmi[r];
-  for (int o = 16; o; o >>= 1) pl0 += __shfl_xor_sync(0xffffffffu, pl0, o);
-  int top[kTop > 0 ? kTop : 1];
+  {  // unpinned stages in order, and the pinned stages' part of the filter bound
+    float p0f = 0.0f;
+    int base = 0;
 #pragma unroll
-  for (int q = 0; q < kTop; q++) top[q] = sw.top[q];
+    for (int slot = 0; slot < 2; slot++) {
+      const int r = lane + 32 * slot;
+      const bool unp = r < S && sw.kma[r] != sw.kmi[r];
+      if (r < S && !unp) p0f += sw.fpr[r] * (float)sw.kmi[r];
+      const unsigned m = __ballot_sync(0xffffffffu, unp);
+      if (unp) sw.ulist[base + __popc(m & ((1u << lane) - 1u))] = (int8_t)r;
+      base += __popc(m);
+    }
+    for (int o = 16; o; o >>= 1) p0f += __shfl_xor_sync(0xffffffffu, p0f, o);
+    if (lane == 0) { sw.nu = base; sw.p0f = p0f; }
+    __syncwarp();
+  }
   int sp = 0;
   // per-candidate filter; survivors are compacted into sw.q and evaluated densely (a warp only
   // saves work when all 32 lanes skip, so skipping must be compacted). A warm-start candidate
@@ -549,16 +587,18 @@ __device__ double cand_main(const InstanceConsts& c, const W& w, SweepSmem<MAXS>
     if (i < n2) {
       tau = cand_tau2<MAXS>(w, sw, i, sp, tau_lo, tau_hi, gen);
       keep = tau >= tau_lo && tau <= tau_hi;
-      if (keep && gen >= 0) {
+      if (keep && gen >= 0) {   // cost >= C tau P(tau) (E >= tau at a certified breakpoint)
         const int g = gen >> 16, m = gen & 0xffff;
         const float tf = (float)tau;
-        float P = pl0 + sw.fpr[g] * (float)(m - sw.kmi[g]);
-#pragma unroll
-        for (int q = 0; q < kTop; q++) {
-          const int r = top[q];
-          if (r < 0 || r == g) continue;
-          const int d = count_lb32(w.stage(r), tf, sw.dom[r]) - sw.kmi[r];
-          if (d > 0) P += sw.fpr[r] * (float)d;
+        // g's class has count m; every other unpinned stage's count is >= its count at tau_hi
+        // (at tau_b when tau <= tau_b) and >= the FP32 lower bound; pinned stages are exact
+        const bool inb = tau <= sw.tb;
+        float P = sw.p0f;
+        for (int j = 0; j < sw.nu; j++) {
+          const int r = sw.ulist[j];
+          const int k = (sw.lead[r] == g) ? m
+                        : max(inb ? (int)sw.kb[r] : sw.kmi[r], count_lb32_est(sw.est[r], tf));
+          P += sw.fpr[r] * (float)k;
         }
         keep = !((double)(fC * tf * P) * (1.0 - 1e-5) > ub + 1e-15);
       }
