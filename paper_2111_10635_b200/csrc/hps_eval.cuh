@@ -69,15 +69,39 @@ struct PlanOut {
 };
 
 // `steps` of the reference's quota bisection (ls/provisioner.py:430-436) once quota_ok(mid) is known to
-// be (mid >= tstar). A step whose midpoint equals a or b is the last that can change anything (the
-// next midpoints repeat it, or a == b), so the loop stops there with the same (a, b) as all steps.
-__device__ __forceinline__ void halvings(double& a, double& b, double tstar, int steps) {
+// be (mid >= tstar); returns the final b (the caller's tau_lo; the final a is not used).
+//  * A step whose midpoint equals a or b is the last that can change b (the next midpoints repeat
+//    it, or a == b), so the loop stops there.
+//  * Once a and b are positive normals of one binade [2^e, 2^(e+1)) with ulp u, a = A u and b = B u,
+//    and every step is exact integer arithmetic: fl(a + b) = 2u round_half_even((A + B) / 2), so
+//    mid = M u with M = round_half_even((A + B) / 2) and the gap d = B - A becomes at most
+//    ceil(d / 2). After ceil(log2 d) + 1 steps the outcome is fixed: b stays when tstar > b (or is
+//    NaN; a alone moves); b = tstar when a < tstar <= b (tstar is then a multiple of u, and the
+//    gap closes onto it); when tstar <= a only b moves, reaches a + u and then takes
+//    M = round_half_even(A + 1/2): b = a for even A, a + u for odd A. With that many steps left
+//    the loop jumps to this end state (bit-identical to running them).
+__device__ __forceinline__ double halvings(double a, double b, double tstar, int steps) {
   for (int it = 0; it < steps; it++) {
+    const long long ia = __double_as_longlong(a), ib = __double_as_longlong(b);
+    const int ea = (int)(ia >> 52);
+    if (ea == (int)(ib >> 52) && ea > 52 && ea < 2047 && ia > 0) {   // one binade, positive normals
+      if (ia == ib) return b;
+      const double u = __longlong_as_double((long long)(ea - 52) << 52);
+      const double d = (b - a) / u;   // exact: Sterbenz, then a power-of-two scale
+      const long long id = __double_as_longlong(d);
+      const int need = (int)(id >> 52) - 1023 + ((id & 0xfffffffffffffLL) != 0) + 1;
+      if (steps - it >= need) {
+        if (!(tstar <= b)) return b;
+        if (tstar <= a) return (ia & 1) ? a + u : a;
+        return tstar;
+      }
+    }
     const double mid = (a + b) / 2.0;
     const bool last = (mid == a) || (mid == b);
     if (mid >= tstar) b = mid; else a = mid;
     if (last) break;
   }
+  return b;
 }
 
 struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min + 1e-15
@@ -353,7 +377,7 @@ __device__ __forceinline__ double bisect_fast(const InstanceConsts& c, const Dev
       lo_bound = x;
     }
     if (lane == 0) HPS_STAT(ST_PROBES_CLOSED, 60 - it);
-    halvings(a, b, tstar, 60 - it);
+    b = halvings(a, b, tstar, 60 - it);
     for (int slot = 0; slot < 2; slot++)
       if (ub[slot] != lb[slot] && b < thr_lb[slot]) lb[slot] = ub[slot];
   }
@@ -547,7 +571,7 @@ __device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W
     tstar = fmax(tstar, tt);
   }
   if (lane == 0) HPS_STAT(ST_PROBES_CLOSED, 60);
-  halvings(a, b, tstar, 60);
+  b = halvings(a, b, tstar, 60);
 #pragma unroll
   for (int slot = 0; slot < 2; slot++)
     kb_out[slot] = (ty[slot] >= 0) ? count_seeded(w.stage(lane + 32 * slot), row[slot], b, kb[slot], (int)c.quota[ty[slot]])

@@ -143,7 +143,7 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
     }
     tstar = fmax(tstar, tt);
   }
-  halvings(a, b, tstar, 60);   // the reference's halvings (ls/provisioner.py:430-436)
+  b = halvings(a, b, tstar, 60);   // the reference's halvings (ls/provisioner.py:430-436)
   kb_out = (ty >= 0) ? count_seeded(w.stage(sl), row, b, kb, (int)c.quota[ty]) : kb;
   return b;
 }
@@ -610,14 +610,17 @@ __device__ __forceinline__ float filter_P(const CandView& v, int g, int m, doubl
       const float B = tf * rb;
       const float h = B - omf;
       if (rb != 0.0f && h > 1e-3f * B) {
+        // count_lb32's bound with fused steps (each rounds once, so the same margins cover it):
+        // ee = 4e-7 (kappa + 2) + 1e-6, lo = q (1 - ee)
         const float rh = rcp_approx_f32(h);
-        const float ee = 4e-7f * (B * rh + 2.0f) + 1e-6f;
-        lo = fmaxf(lo, (frac * rh) * (1.0f - ee));
+        const float ee = __fmaf_rn(4e-7f, B * rh, 1.8e-6f);
+        const float q = frac * rh;
+        lo = fmaxf(lo, __fmaf_rn(-q, ee, q));
       }
     }
     const int fl = (int)((__float_as_uint(b.w) >> sh) & 0xffffu);
     const int k = (v.lead[r] == g) ? m : max(fl, (int)ceilf(lo));
-    P += a.w * (float)k;
+    P = __fmaf_rn(a.w, (float)k, P);
   }
   return P;
 }
