@@ -950,7 +950,7 @@ struct HpsInstance {
   bool fast = false;
   std::vector<StageEntry> h_stages;
   int sm_count = 148;
-  int grid_per_sm = 16;   // blocks per SM of the split kernels' grid (HPS_GRID_PER_SM)
+  int grid_per_sm = 32;   // blocks per SM of the split kernels' grid (HPS_GRID_PER_SM; 16: +2%)
   int carveout = -1;      // shared-memory carveout % for the split kernels (HPS_CARVEOUT)
   size_t te_bytes = 0;    // threshold-table size (bounds of the checked build)
   uint64_t chunk = 0;     // plans per split-kernel chunk (HPS_CHUNK; 0: by MAXS)
