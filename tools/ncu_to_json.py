@@ -24,7 +24,7 @@ METRICS = {
 }
 AVERAGED = {"issue_active_pct", "threads_per_warp_inst", "fp64_pipe_pct"}
 SWEEP_KERNELS = ("stage_kernel", "bisect_kernel", "prep_kernel", "candidate_kernel", "slow_kernel",
-                 "stage_kernel_h", "bisect_kernel_h", "prep_kernel_h",
+                 "stage_kernel_h", "bisect_kernel_h", "prep_kernel_h", "candidate_kernel_h", "init_parts_kernel",
                  "finish_argmin", "merge_argmin")
 
 
