@@ -9,6 +9,9 @@
 // cands_prefix (hps_eval.cuh), so the same bits.
 #pragma once
 
+#ifndef HPS_END_REFINE
+#define HPS_END_REFINE 1   // second grid level refines the end cells of the first (not uniform)
+#endif
 #ifndef HPS_WARM_ROUNDS
 #define HPS_WARM_ROUNDS 1          // warm-start rounds of 16 exact evaluations in cand_prep_half (2: -1.7%)
 #endif
@@ -399,7 +402,8 @@ struct WarpSmemP {
 };
 
 // interval_cells (hps_sweep.cuh) for the plan of this half: segment lane j holds grid point j
-__device__ __noinline__ void interval_cells_half(double t, double L, double d, double thr, double& ta, double& tb) {
+__device__ __noinline__ void interval_cells_half(double t, double L, double d, double thr, double& ta, double& tb,
+                                                 double& ta_in, double& tb_in) {
   const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
   const unsigned am = seg_mask();
   const double t1 = __shfl_down_sync(am, t, 1, 16);
@@ -418,6 +422,9 @@ __device__ __noinline__ void interval_cells_half(double t, double L, double d, d
   const int f = __ffs(mk) - 1, l = 31 - __clz(mk);
   const double nta = __shfl_sync(am, t, base + f);
   tb = __shfl_sync(am, t, base + l + 1);
+  // inner ends of the first and last kept cells (equal to tb / ta when one cell is kept)
+  ta_in = __shfl_sync(am, t, base + f + 1);
+  tb_in = __shfl_sync(am, t, base + l);
   ta = nta;
 }
 
@@ -524,13 +531,27 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
   double ta = tau_lo, tbh = tau_hi;
   if (grid && ub < inf) {
     const double thr = (ub + 1e-15) * (1.0 + 1e-7);
-    interval_cells_half(g_t, g_L, g_d, thr, ta, tbh);
+    double ta_in, tb_in;
+    interval_cells_half(g_t, g_L, g_d, thr, ta, tbh, ta_in, tb_in);
 #pragma unroll 1
     for (int lvl = 1; lvl < HPS_GRID_LEVELS && ta <= tbh; lvl++) {
+#if HPS_END_REFINE
+      // L is convex, so {L <= thr} is one interval whose ends lie in the first and last kept
+      // cells: with more than one kept cell, 8 points refine each end cell (the interior cell
+      // between them keeps its valid tangent bound); one kept cell is refined uniformly
+      double t1;
+      if (ta_in < tbh && tb_in > ta && ta_in <= tb_in) {
+        t1 = (sl < 8) ? ((sl == 7) ? ta_in : ta + (ta_in - ta) * (double)sl * (1.0 / 7))
+                      : ((sl == 15) ? tbh : tb_in + (tbh - tb_in) * (double)(sl - 8) * (1.0 / 7));
+      } else {
+        t1 = grid_point<MAXS>(ta, tbh);
+      }
+#else
       const double t1 = grid_point<MAXS>(ta, tbh);
+#endif
       double L1, d1;
       lb_cont<MAXS>(w, sw, S, c.bo, C, t1, L1, d1, true);
-      interval_cells_half(t1, L1, d1, thr, ta, tbh);
+      interval_cells_half(t1, L1, d1, thr, ta, tbh, ta_in, tb_in);
     }
   }
   // count of every stage at tau_b: a candidate tau <= tau_b has count_r(tau) >= count_r(tau_b)
