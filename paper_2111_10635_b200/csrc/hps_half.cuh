@@ -440,6 +440,9 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
   const int r = sl;
   const bool mine = r < S;
   const bool pinned = mine && (w.kmax[r] == w.kmin[r]);
+  // class leader: the first stage of r's class (one MATCH over the half instead of a scan)
+  const unsigned same = __match_any_sync(am, mine ? w.cls[r] : -1 - sl);
+  const int ld = __ffs(same) - 1 - base;
   if (mine) {
     sw.pr[r] = c.price_s[w.stage(r).type];
     sw.fpr[r] = (float)sw.pr[r];
@@ -448,8 +451,6 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
     sw.etp[r] = pinned ? HPS_TE(w.row[r], (int)w.kmin[r] - 1).et : 0.0;
     sw.dom[r] = pinned ? 0 : side_dominance(w.stage(r), tau_lo, tau_hi, c.bo);
     est_setup<MAXS>(w, sw, r);
-    int ld = 0;
-    while (w.cls[ld] != w.cls[r]) ld++;
     sw.lead[r] = (int8_t)ld;
     sw.gex[r] = (ld == r && !pinned) ? __ldg(tb.gex + w.ent[r]) : 0;
   }
@@ -460,28 +461,8 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
     if (unp) sw.ulist[__popc(m & ((1u << sl) - 1u))] = (int8_t)r;
     if (sl == 0) { sw.nu = __popc(m); sw.p0 = p0; }
   }
-  __syncwarp(am);
-  if (sl == 0) {
-    int t[kTop > 0 ? kTop : 1];
-    double v[kTop > 0 ? kTop : 1];
-#pragma unroll
-    for (int q = 0; q < kTop; q++) { t[q] = -1; v[q] = -1.0; }
-#pragma unroll 1
-    for (int q0 = 0; q0 < S; q0++) {
-      if (w.kmax[q0] == w.kmin[q0]) continue;
-      double vv = sw.pr[q0] * (w.kmax[q0] - w.kmin[q0]);
-      int tt = q0;
-#pragma unroll
-      for (int q = 0; q < kTop; q++) {
-        if (vv > v[q]) {
-          const double v2 = v[q]; const int t2 = t[q];
-          v[q] = vv; t[q] = tt; vv = v2; tt = t2;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kTop; q++) sw.top[q] = t[q];
-  }
+  // (no top-stage list: candidate_kernel_h's filter bounds every unpinned stage)
+  if (sl == 0) sw.top[0] = -1;
   __syncwarp(am);
   const CostScalars cs{c.bo, c.batch, c.work, c.limit};
   const double C = c.work / c.batch;
