@@ -155,20 +155,20 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
 template <class W>
 __device__ void cands_prefix_half(const DeviceTables& tb, W& w, int S, int kb, int& n_cand) {
   const int sl = threadIdx.x & 15, base = threadIdx.x & 16;
+  const unsigned am = seg_mask();
+  const int cl = (sl < S) ? tb_class(tb, w.ent[sl]) : -1 - sl;
   if (sl < S) {
     w.kmax[sl] = kb;
-    w.cls[sl] = tb_class(tb, w.ent[sl]);
+    w.cls[sl] = cl;
   }
-  __syncwarp(seg_mask());
+  // class leader = the first stage of its class (one MATCH over the half)
+  const bool leader = (__ffs(__match_any_sync(am, cl)) - 1 - base) == sl;
+  __syncwarp(am);
   int cnt = 0;
   if (sl < S) {
-    bool leader = true;
-    for (int q = 0; q < sl; q++)
-      if (w.cls[q] == w.cls[sl]) { leader = false; break; }
-    const int span = w.kmax[sl] - w.kmin[sl];
+    const int span = kb - w.kmin[sl];
     if (leader && span <= kBpLimit) cnt = span + 1;
   }
-  const unsigned am = seg_mask();
   int inc = cnt;
 #pragma unroll
   for (int o = 1; o < 16; o <<= 1) {
@@ -796,36 +796,29 @@ __device__ void final_half(const InstanceConsts& c, CandView& v, const StageEntr
   // evaluate(): overall = B / max_s et_s; zero-time stages give inf (ls/costmodel.py:127-128)
   const double overall = (emax > 0) ? c.batch / emax : inf;
   const double exec_time = (overall > 0 && overall != inf) ? c.work / overall : 0.0;
-  // per-type totals, summed over types in order of first occurrence, then the PS type
-  unsigned rem = seg_or(t >= 0 ? 1u << t : 0u);
-  while (rem) {
-    const int ty = __ffs(rem) - 1;
-    rem &= rem - 1;
+  // per-type totals, summed over types in order of first occurrence, then the PS type: the
+  // first-occurrence stages are the lanes that lead their type's MATCH group, visited in order
+  const unsigned same = __match_any_sync(am, t >= 0 ? t : 64 + sl);
+  unsigned fo = seg_ballot(t >= 0 && (__ffs(same) - 1 - base) == sl);
+  double per_second = 0.0;
+  bool first = true, seen_ps = false;
+  while (fo) {
+    const int j = __ffs(fo) - 1;
+    fo &= fo - 1;
+    const int ty = __shfl_sync(am, t, base + j);
     const int tot = seg_sum(t == ty ? k : 0);
-    if (sl == 0) v.tsum[ty] = (unsigned)tot;
+    const double term = c.price_s[ty] * (double)((unsigned long long)(unsigned)tot +
+                                                  (ty == c.ps_type ? (unsigned long long)ps : 0ull));
+    per_second = first ? term : per_second + term;
+    first = false;
+    seen_ps |= (ty == c.ps_type);
   }
-  __syncwarp(am);
-  double cost = 0.0;
-  if (sl == 0) {
-    double per_second = 0.0;
-    unsigned seen = 0;
-    bool first = true;
-#pragma unroll 1
-    for (int s = 0; s < S; s++) {
-      const int ty = v.type[s];
-      if (seen >> ty & 1u) continue;
-      seen |= 1u << ty;
-      const double term = c.price_s[ty] * (double)(v.tsum[ty] + (ty == c.ps_type ? (unsigned long long)ps : 0ull));
-      per_second = first ? term : per_second + term;
-      first = false;
-    }
-    if (ps > 0 && !(seen >> c.ps_type & 1u)) {
-      const double term = c.price_s[c.ps_type] * (double)ps;
-      per_second = first ? term : per_second + term;
-    }
-    cost = exec_time * per_second;
+  if (ps > 0 && !seen_ps) {
+    const double term = c.price_s[c.ps_type] * (double)ps;
+    per_second = first ? term : per_second + term;
   }
-  out.cost = __shfl_sync(am, cost, base);
+  const double cost = exec_time * per_second;
+  out.cost = cost;
   out.status = HPS_ST_OK;
   out.gap = 0.0;
   out.ps = ps;
