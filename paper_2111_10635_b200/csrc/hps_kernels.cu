@@ -2037,8 +2037,14 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   if (const char* e = getenv("HPS_CHUNK")) in->chunk = (uint64_t)std::max(1024ll, atoll(e));
   if (const char* e = getenv("HPS_SUPERCHUNK")) in->super_chunk = (uint64_t)std::max(1ll, std::min(atoll(e), 1ll << 31));
   if (const char* e = getenv("HPS_PIPE")) in->pipe = std::max(1, std::min(2, atoi(e)));
-  if (in->pipe > 1) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&in->aux, cudaStreamNonBlocking));
+  if (in->pipe > 1) {   // one auxiliary stream per device for the process (instances come and go;
+                        // stream order plus the per-instance fork/join events keep each call ordered)
+    static std::mutex mu;
+    static cudaStream_t aux[256] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 0 || dev >= 256) return set_err(HPS_E_CONFIG, "device index out of range");
+    if (!aux[dev]) CUDA_TRY(cudaStreamCreateWithFlags(&aux[dev], cudaStreamNonBlocking));
+    in->aux = aux[dev];
     CUDA_TRY(cudaEventCreateWithFlags(&in->ev_fork, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&in->ev_join, cudaEventDisableTiming));
   }
@@ -2152,7 +2158,6 @@ int hps_instance_destroy(HpsInstance* in) {
   cudaFree(in->d_te);
   cudaFree(in->d_cls);
   cudaFree(in->d_gex);
-  if (in->aux) cudaStreamDestroy(in->aux);
   if (in->ev_fork) cudaEventDestroy(in->ev_fork);
   if (in->ev_join) cudaEventDestroy(in->ev_join);
   delete in;
