@@ -104,6 +104,26 @@ __device__ __forceinline__ double halvings(double a, double b, double tstar, int
   return b;
 }
 
+// For stages r = lane (slot 0) and lane + 32 (slot 1) of an S-stage plan (S <= 64): the first
+// stage with the same key (k0 / k1, keys >= 0). One MATCH per slot; a slot-1 stage whose key also
+// occurs in slot 0 takes the first such slot-0 stage (a 32-shuffle scan, only when S > 32).
+__device__ __forceinline__ void first_same2(int S, int k0, int k1, int& f0, int& f1) {
+  const int lane = threadIdx.x & 31;
+  const int a = (lane < S) ? k0 : -1 - lane;        // absent stages get distinct negative keys
+  const int b = (lane + 32 < S) ? k1 : -33 - lane;
+  f0 = __ffs(__match_any_sync(0xffffffffu, a)) - 1;
+  f1 = 32 + __ffs(__match_any_sync(0xffffffffu, b)) - 1;
+  if (S > 32) {
+    int g = 64;
+#pragma unroll 4
+    for (int q = 0; q < 32; q++) {
+      const int kq = __shfl_sync(0xffffffffu, a, q);
+      if (kq == b && q < g) g = q;
+    }
+    if (g < 64) f1 = g;
+  }
+}
+
 struct TieBuf {  // Pareto set: costs ascending, taus ascending, all <= lane_min + 1e-15
   double c[kTieBuf], t[kTieBuf];
   int n;
@@ -618,13 +638,13 @@ __device__ __forceinline__ void cands_prefix(const DeviceTables& tb, W& w, int S
     }
   }
   __syncwarp();
+  int f[2];
+  first_same2(S, (lane < S) ? w.cls[lane] : 0, (lane + 32 < S) ? w.cls[lane + 32] : 0, f[0], f[1]);
   int cnt[2] = {0, 0};
   for (int slot = 0; slot < 2; slot++) {
     const int s = lane + 32 * slot;
     if (s < S) {
-      bool leader = true;
-      for (int q = 0; q < s; q++)
-        if (w.cls[q] == w.cls[s]) { leader = false; break; }
+      const bool leader = f[slot] == s;   // first stage of its class
       double span = w.kmax[s] - w.kmin[s];
       if (leader && span <= (double)kBpLimit) cnt[slot] = (int)span + 1;
     }
@@ -968,12 +988,17 @@ __device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, W& w, 
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   int accel = 0, on_ps = 0;
   double emax = 0.0;
-#pragma unroll 1
-  for (int s = lane; s < S; s += 32) {
+  int ks[2] = {0, 0}, ts[2] = {-1, -1};   // count and type of stages lane and lane + 32
+#pragma unroll
+  for (int slot = 0; slot < 2; slot++) {
+    const int s = lane + 32 * slot;
+    if (s >= S) continue;
     const int lo = (int)w.kmin[s], hi = (int)w.kmax[s];
     const int k = (lo == hi) ? lo : count_seeded(w.stage(s), w.row[s], tau, lo, hi);
     w.kres[s] = (double)k;
     const int t = w.stage(s).type;
+    ks[slot] = k;
+    ts[slot] = t;
     if (!c.is_cpu[t]) accel += k;
     if (t == c.ps_type) on_ps += k;
     const double et = __ldg(&HPS_TE(w.row[s], k - 1).et);
@@ -998,37 +1023,31 @@ __device__ __forceinline__ void phase_final_fast(const InstanceConsts& c, W& w, 
   // give inf (ls/costmodel.py:127-128)
   const double overall = (emax > 0) ? c.batch / emax : inf;
   const double exec_time = (overall > 0 && overall != inf) ? c.work / overall : 0.0;
-  // per-type totals; the sum runs over types in order of first occurrence, then the PS type
-#pragma unroll 1
-  for (int t = 0; t < c.T; t++) {
-    unsigned v = 0;
-#pragma unroll 1
-    for (int s = lane; s < S; s += 32) v += (w.stage(s).type == t) ? (unsigned)w.kres[s] : 0u;
-    v = __reduce_add_sync(0xffffffffu, v);
-    if (lane == 0) w.tsum[t] = v;
+  // per-type totals; the sum runs over types in order of first occurrence (the stages that lead
+  // their type's MATCH group, visited in stage order), then the PS type
+  int f0, f1;
+  first_same2(S, ts[0], ts[1], f0, f1);
+  unsigned fo0 = __ballot_sync(0xffffffffu, lane < S && f0 == lane);
+  unsigned fo1 = __ballot_sync(0xffffffffu, lane + 32 < S && f1 == lane + 32);
+  double per_second = 0.0;
+  bool first = true, seen_ps = false;
+  while (fo0 | fo1) {
+    int t;
+    if (fo0) { const int j = __ffs(fo0) - 1; fo0 &= fo0 - 1; t = __shfl_sync(0xffffffffu, ts[0], j); }
+    else { const int j = __ffs(fo1) - 1; fo1 &= fo1 - 1; t = __shfl_sync(0xffffffffu, ts[1], j); }
+    const unsigned tot = __reduce_add_sync(0xffffffffu, (ts[0] == t ? (unsigned)ks[0] : 0u) +
+                                                            (ts[1] == t ? (unsigned)ks[1] : 0u));
+    const double term = c.price_s[t] * (double)((unsigned long long)tot + (t == c.ps_type ? (unsigned long long)ps : 0ull));
+    per_second = first ? term : per_second + term;
+    first = false;
+    seen_ps |= (t == c.ps_type);
   }
-  __syncwarp();
-  double cost = 0.0;
-  if (lane == 0) {
-    double per_second = 0.0;
-    unsigned seen = 0;
-    bool first = true;
-#pragma unroll 1
-    for (int s = 0; s < S; s++) {
-      const int t = w.stage(s).type;
-      if (seen >> t & 1u) continue;
-      seen |= 1u << t;
-      const double term = c.price_s[t] * (double)(w.tsum[t] + (t == c.ps_type ? (unsigned long long)ps : 0ull));
-      per_second = first ? term : per_second + term;
-      first = false;
-    }
-    if (ps > 0 && !(seen >> c.ps_type & 1u)) {
-      const double term = c.price_s[c.ps_type] * (double)ps;
-      per_second = first ? term : per_second + term;
-    }
-    cost = exec_time * per_second;
+  if (ps > 0 && !seen_ps) {
+    const double term = c.price_s[c.ps_type] * (double)ps;
+    per_second = first ? term : per_second + term;
   }
-  out.cost = __shfl_sync(0xffffffffu, cost, 0);
+  const double cost = exec_time * per_second;
+  out.cost = cost;
   out.status = HPS_ST_OK;
   out.gap = 0.0;
   out.ps = ps;

@@ -361,6 +361,8 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
                             SweepSmem<MAXS>& sw, int S, double tau_lo, double tau_hi, int n_cand, TieBuf& buf) {
   const int lane = threadIdx.x & 31;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  int fl[2];   // first stage of each stage's class
+  first_same2(S, (lane < S) ? w.cls[lane] : 0, (lane + 32 < S) ? w.cls[lane + 32] : 0, fl[0], fl[1]);
 #pragma unroll 1
   for (int r = lane; r < S; r += 32) {
     const bool pinned = (w.kmax[r] == w.kmin[r]);
@@ -371,8 +373,7 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
     sw.etp[r] = pinned ? w.row[r][(int)w.kmin[r] - 1].et : 0.0;
     sw.dom[r] = pinned ? 0 : side_dominance(w.stage(r), tau_lo, tau_hi, c.bo);
     est_setup<MAXS>(w, sw, r);
-    int ld = 0;  // first stage of r's class
-    while (w.cls[ld] != w.cls[r]) ld++;
+    const int ld = fl[r >> 5];
     sw.lead[r] = (int8_t)ld;
     sw.gex[r] = (ld == r && !pinned) ? __ldg(tb.gex + w.ent[r]) : 0;
   }
