@@ -428,6 +428,32 @@ static __device__ __noinline__ int count_seeded(const StageEntry& s, const TEPai
   return count_tab(row, tau, lo, hi, k);
 }
 
+// the FP32 seed constants of a stage, held in registers across the Newton iterations
+struct SeedConsts {
+  float rb[2], om[2], fr[2];
+  __device__ __forceinline__ void load(const StageEntry& s) {
+    rb[0] = s.f_rbo; rb[1] = s.f_rbd;
+    om[0] = s.f_oma; om[1] = s.f_omb;
+    fr[0] = s.f_alpha; fr[1] = s.f_beta;
+  }
+};
+
+// q_cont from register-held seed constants (same arithmetic)
+__device__ __forceinline__ float q_cont_r(const SeedConsts& s, float tau, float& dq) {
+  float q = 1.0f;
+  dq = 0.0f;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const float rb = s.rb[side], frac = s.fr[side];
+    if (rb == 0.0f || frac == 0.0f) continue;
+    const float h = tau * rb - s.om[side];
+    const float rh = rcp_approx_f32(h);
+    const float v = (h > 0.0f) ? frac * rh : 3.0e38f;
+    if (v > q) { q = v; dq = (h > 0.0f) ? -v * rb * rh : -3.0e38f; }
+  }
+  return q;
+}
+
 // FP32 continuous count q(tau) = max(1, frac / (tau rb - (1 - frac))) of both sides and dq/dtau
 // (seed arithmetic only)
 __device__ __forceinline__ float q_cont(const StageEntry& s, float tau, float& dq) {

@@ -88,9 +88,11 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
     const float target = (float)Q - 0.5f * (float)nst;
     const float flo = (float)lt, fhi = (float)b;
     float x = flo;
+    SeedConsts sc;
+    if (mb) sc.load(w.stage(sl));
     for (int itn = 0; itn < 12; itn++) {
       float F = 0.0f, dF = 0.0f;
-      if (mb) F = q_cont(w.stage(sl), x, dF);
+      if (mb) F = q_cont_r(sc, x, dF);
       F = seg_sumf(F);
       dF = seg_sumf(dF);
       if (fabsf(F - target) <= 0.25f || !(dF < 0.0f) || !(F < 3.0e37f)) break;
