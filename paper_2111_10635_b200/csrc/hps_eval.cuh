@@ -409,6 +409,35 @@ __device__ __forceinline__ double bisect_fast(const InstanceConsts& c, const Dev
 
 // Exact count(tau) of a stage known to lie in [lo, hi] (hi <= table cap): FP32 seed, confirmed by
 // theta(k) <= tau < theta(k - 1) or corrected by the galloping table search.
+// the FP32 seed constants of a stage, held in registers across repeated count searches
+struct SeedConsts {
+  float rb[2], om[2], fr[2];
+  __device__ __forceinline__ void load(const StageEntry& s) {
+    rb[0] = s.f_rbo; rb[1] = s.f_rbd;
+    om[0] = s.f_oma; om[1] = s.f_omb;
+    fr[0] = s.f_alpha; fr[1] = s.f_beta;
+  }
+};
+
+// count_seeded from register-held seed constants (same seed arithmetic, same exact table test)
+static __device__ __noinline__ int count_seeded_r(const SeedConsts sc, const TEPair* row, double tau, int lo, int hi) {
+  const float tf = (float)tau;
+  float q = 1.0f;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const float rb = sc.rb[side], frac = sc.fr[side];
+    if (rb == 0.0f || frac == 0.0f) continue;
+    const float h = tf * rb - sc.om[side];
+    q = (h > 0.0f) ? fmaxf(q, frac * rcp_approx_f32(h)) : 3.0e38f;
+  }
+  int k = (q < 2.0e9f) ? (int)ceilf(q) : hi;
+  k = min(max(k, lo), hi);
+  const double2 pk = __ldg(reinterpret_cast<const double2*>(&HPS_TE(row, k - 1)));  // {et(k), theta(k-1)}
+  const double thk = __ldg(&HPS_TE(row, k).th);
+  if (thk <= tau && tau < pk.y) return k;
+  return count_tab(row, tau, lo, hi, k);
+}
+
 static __device__ __noinline__ int count_seeded(const StageEntry& s, const TEPair* row, double tau, int lo, int hi) {
   const float tf = (float)tau;
   float q = 1.0f;
@@ -427,16 +456,6 @@ static __device__ __noinline__ int count_seeded(const StageEntry& s, const TEPai
   if (thk <= tau && tau < pk.y) return k;
   return count_tab(row, tau, lo, hi, k);
 }
-
-// the FP32 seed constants of a stage, held in registers across the Newton iterations
-struct SeedConsts {
-  float rb[2], om[2], fr[2];
-  __device__ __forceinline__ void load(const StageEntry& s) {
-    rb[0] = s.f_rbo; rb[1] = s.f_rbd;
-    om[0] = s.f_oma; om[1] = s.f_omb;
-    fr[0] = s.f_alpha; fr[1] = s.f_beta;
-  }
-};
 
 // q_cont from register-held seed constants (same arithmetic)
 __device__ __forceinline__ float q_cont_r(const SeedConsts& s, float tau, float& dq) {

@@ -70,6 +70,8 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
   const int ty = (sl < S) ? w.stage(sl).type : -1;
   const int kb = (sl < S) ? kb_in : 0;
   const TEPair* row = (sl < S) ? w.row[sl] : nullptr;
+  SeedConsts sc;   // this lane's stage seed constants, read once for every search below
+  if (sl < S) sc.load(w.stage(sl));
   const unsigned present = seg_or(ty >= 0 ? 1u << ty : 0u);
   double tstar = -inf;
   unsigned rem = present;
@@ -79,7 +81,7 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
     const int Q = (int)c.quota[t];
     const bool mb = ty == t;
     const double lt = seg_max(mb ? __ldg(&HPS_TE(row, Q).th) : -inf);
-    int cnt = mb ? count_seeded(w.stage(sl), row, lt, kb, Q) : 0;
+    int cnt = mb ? count_seeded_r(sc, row, lt, kb, Q) : 0;
     if (seg_sum(cnt) <= Q) {
       tstar = fmax(tstar, lt);
       continue;
@@ -88,8 +90,6 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
     const float target = (float)Q - 0.5f * (float)nst;
     const float flo = (float)lt, fhi = (float)b;
     float x = flo;
-    SeedConsts sc;
-    if (mb) sc.load(w.stage(sl));
     for (int itn = 0; itn < 12; itn++) {
       float F = 0.0f, dF = 0.0f;
       if (mb) F = q_cont_r(sc, x, dF);
@@ -103,7 +103,7 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
       if (done) break;
     }
     const double te = fmin(fmax((double)x, lt), b);
-    cnt = mb ? count_seeded(w.stage(sl), row, te, kb, Q) : 0;
+    cnt = mb ? count_seeded_r(sc, row, te, kb, Q) : 0;
     const int se = seg_sum(cnt);
     double tt;
     if (se <= Q) {   // descending thresholds below te (count increments)
@@ -149,7 +149,7 @@ __device__ double bisect_half(const InstanceConsts& c, const W& w, int S, double
     tstar = fmax(tstar, tt);
   }
   b = halvings(a, b, tstar, 60);   // the reference's halvings (ls/provisioner.py:430-436)
-  kb_out = (ty >= 0) ? count_seeded(w.stage(sl), row, b, kb, (int)c.quota[ty]) : kb;
+  kb_out = (ty >= 0) ? count_seeded_r(sc, row, b, kb, (int)c.quota[ty]) : kb;
   return b;
 }
 
@@ -442,6 +442,8 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
   const int r = sl;
   const bool mine = r < S;
   const bool pinned = mine && (w.kmax[r] == w.kmin[r]);
+  SeedConsts scr;   // stage r's seed constants for the count searches below
+  if (mine) scr.load(w.stage(r));
   // class leader: the first stage of r's class (one MATCH over the half instead of a scan)
   const unsigned same = __match_any_sync(am, mine ? w.cls[r] : -1 - sl);
   const int ld = __ffs(same) - 1 - base;
@@ -483,7 +485,7 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
     if (mine) {
       const int lo = sw.kmi[r], chi = min(sw.kma[r], sw.gex[r]);
       ok = grid && w.pre[r + 1] > w.pre[r] && chi >= lo;
-      if (ok) cstar = min(max(count_seeded(w.stage(r), w.row[r], tstar, lo, sw.kma[r]), lo), chi);
+      if (ok) cstar = min(max(count_seeded_r(scr, w.row[r], tstar, lo, sw.kma[r]), lo), chi);
     }
     const unsigned lm = seg_ballot(ok);
     const int nl = __popc(lm);
@@ -540,7 +542,7 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
   // count of every stage at tau_b: a candidate tau <= tau_b has count_r(tau) >= count_r(tau_b)
   // for every r (counts are non-increasing), the candidate filter's base (cand_main_half)
   kbv = mine ? sw.kmi[r] : 0;
-  if (mine && !pinned && ta <= tbh) kbv = count_seeded(w.stage(r), w.row[r], tbh, sw.kmi[r], sw.kma[r]);
+  if (mine && !pinned && ta <= tbh) kbv = count_seeded_r(scr, w.row[r], tbh, sw.kmi[r], sw.kma[r]);
   tb_out = (ta <= tbh) ? tbh : -inf;
   if (mine) {
     if (w.pre[r + 1] > w.pre[r]) {  // class leader with breakpoints
@@ -549,7 +551,7 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
       const int chi = min(hi, sw.gex[r]);
       if (ta <= tbh && chi >= lo) {
         const int ma = kbv;
-        const int mb = count_seeded(w.stage(r), w.row[r], ta, lo, hi);
+        const int mb = count_seeded_r(scr, w.row[r], ta, lo, hi);
         alo = max(ma, lo);
         an = max(0, min(mb, chi) - alo + 1);
       }
