@@ -776,7 +776,15 @@ __device__ void final_half(const InstanceConsts& c, CandView& v, const StageEntr
   k = 0;
   if (sl < S) {
     const int lo = v.kmi[sl], hi = v.kma[sl];
-    k = (lo == hi) ? lo : count_seeded(*st, v.row[sl], tau, lo, hi);
+    if (lo == hi) {
+      k = lo;
+    } else {   // seed constants from the view (a dominated side is off: still a valid seed)
+      SeedConsts sc;
+      const float4 a = v.fe[sl][0], b = v.fe[sl][1];
+      sc.rb[0] = a.x; sc.om[0] = a.y; sc.fr[0] = a.z;
+      sc.rb[1] = b.x; sc.om[1] = b.y; sc.fr[1] = b.z;
+      k = count_seeded_r(sc, v.row[sl], tau, lo, hi);
+    }
     t = v.type[sl];
     if (!c.is_cpu[t]) accel = k;
     if (t == c.ps_type) on_ps = k;
