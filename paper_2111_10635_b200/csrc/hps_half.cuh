@@ -447,20 +447,29 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
   // class leader: the first stage of r's class (one MATCH over the half instead of a scan)
   const unsigned same = __match_any_sync(am, mine ? w.cls[r] : -1 - sl);
   const int ld = __ffs(same) - 1 - base;
+  double prr = 0.0;
   if (mine) {
-    sw.pr[r] = c.price_s[w.stage(r).type];
-    sw.fpr[r] = (float)sw.pr[r];
+    prr = c.price_s[w.stage(r).type];
+    sw.pr[r] = prr;
+    sw.fpr[r] = (float)prr;
     sw.kmi[r] = (int)w.kmin[r];
     sw.kma[r] = (int)w.kmax[r];
-    sw.etp[r] = pinned ? HPS_TE(w.row[r], (int)w.kmin[r] - 1).et : 0.0;
-    sw.dom[r] = pinned ? 0 : side_dominance(w.stage(r), tau_lo, tau_hi, c.bo);
-    est_setup<MAXS>(w, sw, r);
+    sw.etp[r] = pinned ? __ldg(&HPS_TE(w.row[r], (int)w.kmin[r] - 1).et) : 0.0;
+    const int dom = pinned ? 0 : side_dominance(w.stage(r), tau_lo, tau_hi, c.bo);
+    sw.dom[r] = dom;
+#pragma unroll
+    for (int side = 0; side < 2; side++) {   // est_setup (hps_sweep.cuh) from the register copy
+      const bool on = (dom != 2 - side) && scr.rb[side] != 0.0f && scr.fr[side] != 0.0f;
+      sw.est[r][3 * side + 0] = on ? scr.rb[side] : 0.0f;
+      sw.est[r][3 * side + 1] = on ? scr.om[side] : -1.0f;
+      sw.est[r][3 * side + 2] = on ? scr.fr[side] : 0.0f;
+    }
     sw.lead[r] = (int8_t)ld;
     sw.gex[r] = (ld == r && !pinned) ? __ldg(tb.gex + w.ent[r]) : 0;
   }
   {  // unpinned stages in order, and the pinned stages' part of the bound
     const bool unp = mine && !pinned;
-    const double p0 = seg_sumd((mine && pinned) ? c.price_s[w.stage(r).type] * w.kmin[r] : 0.0);
+    const double p0 = seg_sumd((mine && pinned) ? prr * w.kmin[r] : 0.0);
     const unsigned m = seg_ballot(unp);
     if (unp) sw.ulist[__popc(m & ((1u << sl) - 1u))] = (int8_t)r;
     if (sl == 0) { sw.nu = __popc(m); sw.p0 = p0; }
