@@ -474,8 +474,6 @@ __device__ double cand_prep_half(const InstanceConsts& c, const DeviceTables& tb
     if (unp) sw.ulist[__popc(m & ((1u << sl) - 1u))] = (int8_t)r;
     if (sl == 0) { sw.nu = __popc(m); sw.p0 = p0; }
   }
-  // (no top-stage list: candidate_kernel_h's filter bounds every unpinned stage)
-  if (sl == 0) sw.top[0] = -1;
   __syncwarp(am);
   const CostScalars cs{c.bo, c.batch, c.work, c.limit};
   const double C = c.work / c.batch;

@@ -1011,8 +1011,7 @@ struct Cont {
 template <int MAXS>
 struct __align__(16) PrepState {
   double ub;
-  double tb;      // right end of the restricted interval (half-warp kernels; -inf: none)
-  int32_t top;
+  double tb;      // right end of the restricted interval (-inf: none)
   int8_t dom[MAXS], lead[MAXS];
   int16_t alo[MAXS], an[MAXS], blo[MAXS];
   int16_t kb[MAXS];   // count at tb (half-warp kernels)
@@ -1312,7 +1311,6 @@ prep_kernel_h(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepStat
       if (sl == 0) {
         out.ub = ub;
         out.tb = tbv;
-        out.top = sw.top[0];
       }
     }
     __syncwarp(seg_mask());
@@ -1576,7 +1574,6 @@ prep_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, PrepState<
     if (lane == 0) {
       out.ub = ub;
       out.tb = sw.tb;
-      out.top = sw.top[0];
     }
     __syncwarp();
   }
@@ -1636,7 +1633,6 @@ candidate_kernel(const InstanceConsts c, const DeviceTables tb, Cont cont, const
       sw.kb[r] = pp.kb[r];
     }
     if (lane == 0) {
-      sw.top[0] = pp.top;
       sw.tb = pp.tb;
     }
     __syncwarp();

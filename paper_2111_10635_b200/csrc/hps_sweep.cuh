@@ -24,11 +24,6 @@
 
 namespace hps {
 
-#ifndef HPS_TOP
-#define HPS_TOP 1
-#endif
-constexpr int kTop = HPS_TOP;   // unpinned stages bounded per candidate (count_lb32)
-
 struct CandQueue {    // survivors of cand_main's lower-bound filter, evaluated 32 at a time
   double q[64];
   int32_t qg[64];      // their generator: (leader << 16) | m, or -1 (tau_lo / tau_hi)
@@ -44,7 +39,6 @@ struct SweepSmem {   // per-warp, per-plan constants of the fast candidate phase
   int32_t alo[MAXS], an[MAXS], blo[MAXS];  // restricted candidate ranges (cand_tau2)
   int32_t pre2[MAXS + 1];
 
-  int32_t top[kTop > 0 ? kTop : 1]; // unpinned stages with the largest price-weighted count span (-1: none)
   int32_t dom[MAXS]; // side_dominance over [tau_lo, tau_hi]: 1 oct, 2 odt, 0 both
   float est[MAXS][6];  // count_est seed constants (est_setup)
   int8_t lead[MAXS]; // class leader of stage r (stages of one class have identical counts)
@@ -394,25 +388,6 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
   }
   __syncwarp();
   if (lane == 0) {
-    int t[kTop > 0 ? kTop : 1];
-    double v[kTop > 0 ? kTop : 1];
-#pragma unroll
-    for (int q = 0; q < kTop; q++) { t[q] = -1; v[q] = -1.0; }
-#pragma unroll 1
-    for (int r = 0; r < S; r++) {
-      if (w.kmax[r] == w.kmin[r]) continue;
-      double vv = sw.pr[r] * (w.kmax[r] - w.kmin[r]);
-      int tt = r;
-#pragma unroll
-      for (int q = 0; q < kTop; q++) {   // insertion into the descending top list
-        if (vv > v[q]) {
-          const double v2 = v[q]; const int t2 = t[q];
-          v[q] = vv; t[q] = tt; vv = v2; tt = t2;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kTop; q++) sw.top[q] = t[q];
     HPS_STAT(ST_NCAND, n_cand);
     HPS_STAT(ST_PLANS_FAST, 1);
     HPS_STAT(ST_STAGES, S);
