@@ -12,13 +12,14 @@
 //    count(b) and count(a). Once every unpinned stage is within one step, quota_ok on (a, b)
 //    switches at one of the thresholds theta_r(count(b)); that switch point tau* is found
 //    exactly and the remaining bisection steps are comparisons mid >= tau*.
-//  * _best_candidate (ls/provisioner.py:262-314): candidates round-robin over lanes; counts are
-//    CERTIFIED arithmetic counts (reciprocal + rigorous error bound, count_cert) with the exact
-//    table search as fallback; a warm start plus a rigorous lower bound (E >= tau at a certified
-//    breakpoint, per-round exact counts at the round's largest tau, FP32 bounds of the top
-//    stage) skips the candidates that cannot reach the minimum or its 1e-15 tie window;
-//    evaluated candidates use the reference's exact sequential per_second sum and its two cost
-//    divisions.
+//  * _best_candidate (ls/provisioner.py:262-314): candidates round-robin over lanes; exact counts
+//    come from an FP32 seed verified against the threshold table; a warm start around the
+//    minimiser of a convex lower bound gives an upper bound ub, the bound confines the certified
+//    candidates that can reach ub + 1e-15 to an interval, and a rigorous per-candidate lower
+//    bound (E >= tau at a certified breakpoint, every unpinned stage's count bounded below in FP32
+//    with its error margin, floored by its count at the interval's end) skips the candidates that
+//    cannot reach the minimum or its 1e-15 tie window; evaluated candidates use the reference's
+//    exact sequential per_second sum and its two cost divisions.
 #pragma once
 #include "hps_eval.cuh"
 
@@ -336,14 +337,15 @@ __device__ __noinline__ double overflow_pass(const CostScalars cs, const W& w, c
 }
 
 // _best_candidate: round-robin candidates over lanes. A warm-start round evaluates 32 candidates
-// around the grid minimiser of the convex bound L exactly (upper bound ub on the minimum). L
+// (16 in the half-warp prep) around the grid minimiser of the convex bound L exactly (upper bound
+// ub on the minimum). L
 // (lb_cont) then confines every certified breakpoint that could reach ub + 1e-15 to an
 // interval [ta, tb] (two grid levels, interval_cells); for each class leader those are the m in
 // [count(tb), count(ta)] (certified: count(et(m)) == m, counts non-increasing). Only these,
 // tau_lo, tau_hi and the uncertified breakpoints remain; each gets a per-candidate bound
-// (E >= tau, the generator's count m, the top stage's FP32 count bound, count(tau_hi) for the
-// others; FP32 slack 1e-5) and is evaluated exactly only when the bound does not exceed the best
-// cost so far + 1e-15. A skipped candidate costs more than the final minimum + 1e-15: it is
+// (E >= tau, the generator's class at count m, every other unpinned stage at the larger of its
+// FP32 count lower bound and its count at tb (tau <= tb) or tau_hi; FP32 slack 1e-5) and is
+// evaluated exactly only when the bound does not exceed the best cost so far + 1e-15. A skipped candidate costs more than the final minimum + 1e-15: it is
 // neither the minimum nor a tie.
 // Part 1 (cand_prep): per-plan constants, warm start, interval and restricted ranges (alo, an,
 // blo); returns ub. Part 2 (cand_main): the filter and exact evaluation over the restricted list.
