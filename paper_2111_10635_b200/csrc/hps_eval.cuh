@@ -511,12 +511,14 @@ __device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   int ty[2], kb[2];
   const TEPair* row[2];
+  SeedConsts sc[2];   // the stages' seed constants, read once for every search below
 #pragma unroll
   for (int slot = 0; slot < 2; slot++) {
     const int s = lane + 32 * slot;
     ty[slot] = (s < S) ? w.stage(s).type : -1;
     kb[slot] = (s < S) ? (int)kb_in[slot] : 0;
     row[slot] = (s < S) ? rows[s] : nullptr;
+    if (s < S) sc[slot].load(w.stage(s));
   }
   const unsigned present =
       __reduce_or_sync(0xffffffffu, (ty[0] >= 0 ? 1u << ty[0] : 0u) | (ty[1] >= 0 ? 1u << ty[1] : 0u));
@@ -536,7 +538,7 @@ __device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W
     int cnt[2] = {0, 0};
 #pragma unroll
     for (int slot = 0; slot < 2; slot++)
-      if (mb[slot]) cnt[slot] = count_seeded(w.stage(lane + 32 * slot), row[slot], lt, kb[slot], Q);
+      if (mb[slot]) cnt[slot] = count_seeded_r(sc[slot], row[slot], lt, kb[slot], Q);
     const int sl = (int)__reduce_add_sync(0xffffffffu, (unsigned)(cnt[0] + cnt[1]));
     if (sl <= Q) {
       tstar = fmax(tstar, lt);
@@ -555,7 +557,7 @@ __device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W
       for (int slot = 0; slot < 2; slot++)
         if (mb[slot]) {
           float d;
-          F += q_cont(w.stage(lane + 32 * slot), x, d);
+          F += q_cont_r(sc[slot], x, d);
           dF += d;
         }
       for (int o = 16; o; o >>= 1) {
@@ -573,7 +575,7 @@ __device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W
     // ---- exact counts at te and exact selection of tau*_t ----
 #pragma unroll
     for (int slot = 0; slot < 2; slot++)
-      if (mb[slot]) cnt[slot] = count_seeded(w.stage(lane + 32 * slot), row[slot], te, kb[slot], Q);
+      if (mb[slot]) cnt[slot] = count_seeded_r(sc[slot], row[slot], te, kb[slot], Q);
     const int se = (int)__reduce_add_sync(0xffffffffu, (unsigned)(cnt[0] + cnt[1]));
     double tt;
     if (se <= Q) {
@@ -639,7 +641,7 @@ __device__ __forceinline__ double bisect_direct(const InstanceConsts& c, const W
   b = halvings(a, b, tstar, 60);
 #pragma unroll
   for (int slot = 0; slot < 2; slot++)
-    kb_out[slot] = (ty[slot] >= 0) ? count_seeded(w.stage(lane + 32 * slot), row[slot], b, kb[slot], (int)c.quota[ty[slot]])
+    kb_out[slot] = (ty[slot] >= 0) ? count_seeded_r(sc[slot], row[slot], b, kb[slot], (int)c.quota[ty[slot]])
                                    : kb[slot];
   return b;
 }

@@ -463,9 +463,11 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
       const int r = lane + 32 * slot;
       // count at tau_b of every stage: a candidate tau <= tau_b has count_r(tau) >= it
       int kbv = 0;
+      SeedConsts scr;   // stage r's seed constants for both searches
       if (r < S) {
+        scr.load(w.stage(r));
         kbv = sw.kmi[r];
-        if (sw.kma[r] != sw.kmi[r] && ta <= tbh) kbv = count_seeded(w.stage(r), w.row[r], tbh, sw.kmi[r], sw.kma[r]);
+        if (sw.kma[r] != sw.kmi[r] && ta <= tbh) kbv = count_seeded_r(scr, w.row[r], tbh, sw.kmi[r], sw.kma[r]);
         sw.kb[r] = (int16_t)kbv;
       }
       if (r < S && w.pre[r + 1] > w.pre[r]) {  // class leader with breakpoints
@@ -474,7 +476,7 @@ __device__ double cand_prep(const InstanceConsts& c, const DeviceTables& tb, con
         const int chi = min(hi, sw.gex[r]);   // certified part [lo, chi]
         if (ta <= tbh && chi >= lo) {
           const int ma = kbv;  // smallest certified m
-          const int mb = count_seeded(w.stage(r), w.row[r], ta, lo, hi);   // largest certified m
+          const int mb = count_seeded_r(scr, w.row[r], ta, lo, hi);   // largest certified m
           alo = max(ma, lo);
           an = max(0, min(mb, chi) - alo + 1);
         }
