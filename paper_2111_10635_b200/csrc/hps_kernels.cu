@@ -960,6 +960,8 @@ struct HpsInstance {
   bool half_cand = true;    // L <= 16: two plans per warp in the candidate kernel (HPS_HALF_CAND=0: one)
   int slow_per_sm = -1;   // resident slow_kernel blocks per SM (occupancy API, first use)
   uint64_t super_chunk = 1ull << 26;  // plans per pending-list pass (HPS_SUPERCHUNK; tests shrink it)
+  int dev = 0;               // device the tables live on
+  size_t sz_stages = 0, sz_stage0 = 0, sz_cls = 0, sz_gex = 0;   // table sizes (allocation cache)
   int pipe = 2;              // split-kernel chunk pipeline streams (HPS_PIPE=1: one stream)
   uint64_t pipe_chunk = 1ull << 20;    // L <= 16 chunk size when pipelined (HPS_CHUNK overrides)
   cudaStream_t aux = nullptr;          // the pipeline's second stream
@@ -2021,6 +2023,42 @@ int hps_instance_create(const HpsInstanceDesc* d, HpsInstance** out) {
 }  // extern "C"
 
 namespace {
+// Device buffers of destroyed instances are kept (per device and size, up to 2 GB) and handed to
+// the next instance of the same shape: re-staging an instance (the e2e path does it every call)
+// then allocates nothing. Buffers enter the cache after a device synchronisation, so no queued
+// kernel of the old instance can still read them.
+std::mutex g_buf_mu;
+std::multimap<std::pair<int, size_t>, void*> g_buf_cache;
+size_t g_buf_bytes = 0;
+constexpr size_t kBufCacheCap = 2ull << 30;
+
+cudaError_t cached_alloc(void** p, size_t n, int dev) {
+  {
+    std::lock_guard<std::mutex> lock(g_buf_mu);
+    auto it = g_buf_cache.find({dev, n});
+    if (it != g_buf_cache.end()) {
+      *p = it->second;
+      g_buf_cache.erase(it);
+      g_buf_bytes -= n;
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(p, n);
+}
+
+void cached_release(void* p, size_t n, int dev) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lock(g_buf_mu);
+    if (g_buf_bytes + n <= kBufCacheCap) {
+      g_buf_cache.insert({{dev, n}, p});
+      g_buf_bytes += n;
+      return;
+    }
+  }
+  cudaFree(p);
+}
+
 int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& d_raw) {
   const int L = d->num_layers, T = d->num_types;
   cudaDeviceGetAttribute(&in->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -2087,6 +2125,7 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   in->fast = fast && (getenv("HPS_FORCE_LITERAL") == nullptr);
   // raw tables -> device
   const size_t tl = (size_t)T * L * sizeof(double);
+  in->dev = dev;
   CUDA_TRY(cudaMalloc(&d_raw, 4 * tl));
   CUDA_TRY(cudaMemcpy(d_raw, d->oct, tl, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy((char*)d_raw + tl, d->odt, tl, cudaMemcpyHostToDevice));
@@ -2094,13 +2133,16 @@ int instance_build(const HpsInstanceDesc* d, HpsInstance* in, int dev, double*& 
   CUDA_TRY(cudaMemcpy((char*)d_raw + 3 * tl, d->beta, tl, cudaMemcpyHostToDevice));
   RawTables raw{d_raw, d_raw + T * L, d_raw + 2 * T * L, d_raw + 3 * T * L};
   const int ne = T * c.P;
-  CUDA_TRY(cudaMalloc(&in->d_stages, sizeof(StageEntry) * ne));
-  CUDA_TRY(cudaMalloc(&in->d_stage0, sizeof(Stage0Info) * T * L));
-  CUDA_TRY(cudaMalloc(&in->d_te, sizeof(TEPair) * off));
+  in->sz_stages = sizeof(StageEntry) * ne;
+  in->sz_stage0 = sizeof(Stage0Info) * T * L;
   in->te_bytes = sizeof(TEPair) * off;
+  in->sz_cls = in->sz_gex = sizeof(int32_t) * ne;
+  CUDA_TRY(cached_alloc(reinterpret_cast<void**>(&in->d_stages), in->sz_stages, dev));
+  CUDA_TRY(cached_alloc(reinterpret_cast<void**>(&in->d_stage0), in->sz_stage0, dev));
+  CUDA_TRY(cached_alloc(reinterpret_cast<void**>(&in->d_te), in->te_bytes, dev));
   if (int rc = chk_bind(in, 0)) return rc;
-  CUDA_TRY(cudaMalloc(&in->d_cls, sizeof(int32_t) * ne));
-  CUDA_TRY(cudaMalloc(&in->d_gex, sizeof(int32_t) * ne));
+  CUDA_TRY(cached_alloc(reinterpret_cast<void**>(&in->d_cls), in->sz_cls, dev));
+  CUDA_TRY(cached_alloc(reinterpret_cast<void**>(&in->d_gex), in->sz_gex, dev));
   HPS_COUNT_LAUNCH();
   stage_table_kernel<<<(ne + 127) / 128, 128>>>(c, raw, in->d_stages);
   CUDA_TRY(cudaGetLastError());
@@ -2149,11 +2191,16 @@ extern "C" {
 
 int hps_instance_destroy(HpsInstance* in) {
   if (!in) return HPS_OK;
-  cudaFree(in->d_stages);
-  cudaFree(in->d_stage0);
-  cudaFree(in->d_te);
-  cudaFree(in->d_cls);
-  cudaFree(in->d_gex);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(in->dev);
+  cudaDeviceSynchronize();   // nothing queued may still read the tables once they are reused
+  cached_release(in->d_stages, in->sz_stages, in->dev);
+  cached_release(in->d_stage0, in->sz_stage0, in->dev);
+  cached_release(in->d_te, in->te_bytes, in->dev);
+  cached_release(in->d_cls, in->sz_cls, in->dev);
+  cached_release(in->d_gex, in->sz_gex, in->dev);
+  cudaSetDevice(cur);
   if (in->ev_fork) cudaEventDestroy(in->ev_fork);
   if (in->ev_join) cudaEventDestroy(in->ev_join);
   delete in;
